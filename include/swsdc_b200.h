@@ -1,0 +1,90 @@
+/*
+ * swsdc_b200.h -- C ABI of the B200 (sm_100a) MLSDC-SH hot path.
+ *
+ * Drop-in boundary for the reference package `swsdc` (/root/reference/pkg/src/swsdc).
+ * The reference has no FFI: its boundary is duck-typed Python objects.  Each
+ * entry point below replaces one reference method; the Python mirror in
+ * paper_1805_07923_b200/ (spharm.py, swe.py, implicit.py, sdc.py, mlsdc.py)
+ * binds these symbols with ctypes and keeps the reference's names, argument
+ * meaning and exceptions.
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers owned by the caller.
+ *   - Spectral arrays: complex128 (interleaved re, im doubles), dense
+ *     triangular layout [r][s], (R+1) x (R+1) per field, zeros for s < r
+ *     (spharm.py:6-10).  A prognostic state is 3 such fields
+ *     (phi_prime, zeta, delta) back to back (swe.py:44-58).
+ *   - Grid arrays: float64 (n_lon, n_lat), longitude-major, latitudes ascending
+ *     in mu (spharm.py:3-5).
+ *   - `batch` independent fields / states are contiguous.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *     stream-ordered and asynchronous; a plan's scratch workspace serialises
+ *     calls that share the plan, so use one plan per concurrent stream.
+ *   - Return value: 0 ok, 1 usage error (-> ValueError), 2 numerical error
+ *     (-> RuntimeError), 3 CUDA error.  swsdc_last_error() describes the last
+ *     failure of the calling thread.
+ */
+#ifndef SWSDC_B200_H
+#define SWSDC_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct swsdc_plan swsdc_plan;
+
+/* Model constants in the order (radius, omega, gravity, nu, h_bar); phi_bar = gravity * h_bar
+ * (swe.py:20-41). */
+typedef struct swsdc_params {
+  double radius, omega, gravity, nu, h_bar;
+} swsdc_params;
+
+const char* swsdc_last_error(void);
+const char* swsdc_version(void);
+
+/* TransformPlan.__init__ (spharm.py:189-206): validates the truncation, builds
+ * the device recurrence tables, checkpoint seeds and FFT twiddles.  mu, w are
+ * HOST arrays of the n_lat Gauss nodes / weights (spharm.py:52-86). */
+int swsdc_plan_create(int truncation, int n_lon, int n_lat, const double* mu, const double* w,
+                      swsdc_plan** out);
+int swsdc_plan_destroy(swsdc_plan* plan);
+/* Pre-size the scratch workspace for up to `fields` simultaneous fields (so no
+ * allocation happens later, e.g. during CUDA graph capture). */
+int swsdc_plan_reserve(swsdc_plan* plan, int fields);
+
+/* TransformPlan.synthesize (spharm.py:258-260); coefficients at truncation
+ * r_in <= R are zero-padded (spharm.py:242-250). */
+int swsdc_synthesize(swsdc_plan* plan, const double* coeffs, int r_in, int batch, double* grid,
+                     void* stream);
+/* TransformPlan.analyze (spharm.py:254-256). */
+int swsdc_analyze(swsdc_plan* plan, const double* grid, int batch, double* coeffs, void* stream);
+/* TransformPlan.synthesize_pair_cos_gradient (spharm.py:262-279), unit sphere. */
+int swsdc_synthesize_uv(swsdc_plan* plan, const double* psi, const double* chi, int r_in, int batch,
+                        double* u, double* v, void* stream);
+/* TransformPlan.analyze_vector_div_curl (spharm.py:281-300), unit sphere. */
+int swsdc_analyze_divcurl(swsdc_plan* plan, const double* u, const double* v, int batch,
+                          double* div, double* curl, void* stream);
+
+/* ShallowWaterRHS.eval_f_e (swe.py:251-279) for `batch` states. */
+int swsdc_eval_fe(swsdc_plan* plan, const swsdc_params* params, int include_nonlinear,
+                  const double* state, int batch, double* out, void* stream);
+/* ShallowWaterRHS.eval_f_i / eval_l_g (swe.py:206-217, 246-249). */
+int swsdc_eval_fi(int truncation, const swsdc_params* params, const double* state, int batch,
+                  double* out, void* stream);
+/* implicit.solve_implicit (implicit.py:31-49): (I - beta F_I) theta = b.  Returns 1
+ * for beta < 0 and 2 when any 2x2 determinant is <= 0. */
+int swsdc_solve_implicit(int truncation, const swsdc_params* params, double beta, const double* b,
+                         int batch, double* out, void* stream);
+
+/* out[i] = sum_k w[k] * x[k][i] over `count` doubles, n <= 32
+ * (sdc._combine sdc.py:211-220 and PrognosticState algebra swe.py:77-102). */
+int swsdc_combine(int n, const double* const* x, const double* w, long long count, double* out,
+                  void* stream);
+/* spharm.truncate / spharm.pad (spharm.py:331-349) over `nmat` (R+1)^2 matrices. */
+int swsdc_resize(const double* in, int r_in, double* out, int r_out, long long nmat, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SWSDC_B200_H */

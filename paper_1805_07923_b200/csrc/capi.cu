@@ -1,0 +1,474 @@
+// C ABI (include/swsdc_b200.h): plan construction and the host-side
+// orchestration of the kernels for each reference entry point.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "fourier.cuh"
+#include "legendre.cuh"
+#include "spectral.cuh"
+#include "../../include/swsdc_b200.h"
+
+namespace swsdc {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+}  // namespace swsdc
+
+using namespace swsdc;
+
+struct swsdc_plan {
+  PlanDev dev{};
+  std::vector<void*> owned;
+  int2* work[2] = {nullptr, nullptr};  // analysis work lists for smax = R, R + 1
+  int nwork[2] = {0, 0};
+  int ldy = 0;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+};
+
+namespace {
+
+template <typename T>
+int upload(swsdc_plan* p, const std::vector<T>& h, T** d) {
+  void* ptr = nullptr;
+  SW_CUDA(cudaMalloc(&ptr, h.size() * sizeof(T) + 16));
+  p->owned.push_back(ptr);
+  SW_CUDA(cudaMemcpy(ptr, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  *d = reinterpret_cast<T*>(ptr);
+  return kOk;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+size_t field_bytes(const swsdc_plan* p) {
+  const PlanDev& P = p->dev;
+  return (size_t)(P.R + 1) * P.Jh * 2 * sizeof(double2);
+}
+size_t y_bytes(const swsdc_plan* p) {
+  return (size_t)(p->dev.R + 1) * p->ldy * sizeof(double2);
+}
+
+int ensure_ws(swsdc_plan* p, int n_eo, int n_x, int n_y, cudaStream_t st = 0) {
+  const size_t need = (size_t)(n_eo + n_x) * field_bytes(p) + (size_t)n_y * y_bytes(p) + 256;
+  if (need <= p->ws_bytes) return kOk;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  // growing the workspace cannot happen during graph capture
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+    set_error("workspace too small during stream capture; call swsdc_plan_reserve first");
+    return kUsage;
+  }
+  if (p->ws) {
+    SW_CUDA(cudaDeviceSynchronize());
+    SW_CUDA(cudaFree(p->ws));
+    p->ws = nullptr;
+    p->ws_bytes = 0;
+  }
+  SW_CUDA(cudaMalloc(&p->ws, need));
+  p->ws_bytes = need;
+  return kOk;
+}
+
+double2* ws_eo(swsdc_plan* p) { return reinterpret_cast<double2*>(p->ws); }
+double2* ws_x(swsdc_plan* p, int n_eo) {
+  return reinterpret_cast<double2*>(p->ws + (size_t)n_eo * field_bytes(p));
+}
+double2* ws_y(swsdc_plan* p, int n_eo, int n_x) {
+  return reinterpret_cast<double2*>(p->ws + (size_t)(n_eo + n_x) * field_bytes(p));
+}
+
+ModelConsts consts(const swsdc_params* q) {
+  ModelConsts c;
+  c.radius = q->radius;
+  c.omega = q->omega;
+  c.gravity = q->gravity;
+  c.nu = q->nu;
+  c.h_bar = q->h_bar;
+  c.phi_bar = q->gravity * q->h_bar;
+  return c;
+}
+
+int check_params(const swsdc_params* q) {
+  if (!q) { set_error("params is NULL"); return kUsage; }
+  if (!(q->radius > 0) || !(q->gravity > 0) || !(q->h_bar > 0)) {
+    set_error("radius, gravity and h_bar must be positive");
+    return kUsage;
+  }
+  if (q->nu < 0) { set_error("diffusion coefficient must be non-negative"); return kUsage; }
+  return kOk;
+}
+
+// Plain synthesis of `batch` fields from coeffs at truncation r_in into eo.
+int syn_plain(swsdc_plan* p, const double2* coeffs, int r_in, int batch, double2* eo,
+              cudaStream_t st) {
+  const PlanDev& P = p->dev;
+  const long long cin = (long long)(r_in + 1) * (r_in + 1);
+  const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
+  int B = 0;
+  for (int cand = 8; cand >= 4; --cand)
+    if (batch % cand == 0) { B = cand; break; }
+  int done = 0;
+  while (done < batch) {
+    int b = B;
+    int groups;
+    if (b == 0) {
+      const int ng = (batch - done + 7) / 8;
+      b = (batch - done + ng - 1) / ng;
+    }
+    groups = (batch - done) / b;
+    if (groups == 0) { b = batch - done; groups = 1; }
+    SynArgs a{};
+    a.src = coeffs + done * cin;
+    a.src_fstride = cin;
+    a.src_R = r_in;
+    a.smax = P.R;
+    a.eo = eo + done * fstride;
+    a.src_mstride = cin * b;
+    a.eo_mstride = fstride * b;
+    a.nmembers = groups;
+    SW_TRY(launch_synthesis(P, a, b, kSynPlain, st));
+    done += b * groups;
+  }
+  return kOk;
+}
+
+// Legendre analysis of nv vectors per member into out (dense or Y scratch).
+int ana_run(swsdc_plan* p, const double2* x, int nv, long long x_mstride, int nmembers,
+            double2* out, long long out_vstride, long long out_rstride, long long out_mstride,
+            int smax, bool zero_fill, cudaStream_t st) {
+  const PlanDev& P = p->dev;
+  const int which = (smax == P.R) ? 0 : 1;
+  const long long vstride_x = (long long)(P.R + 1) * P.Jh * 2;
+  for (int v0 = 0; v0 < nv; v0 += 16) {
+    AnaArgs a{};
+    a.nv = (nv - v0 < 16) ? nv - v0 : 16;
+    a.x = x + v0 * vstride_x;
+    a.out = out + v0 * out_vstride;
+    a.out_vstride = out_vstride;
+    a.out_rstride = out_rstride;
+    a.smax = smax;
+    a.zero_fill = zero_fill ? 1 : 0;
+    a.work = p->work[which];
+    a.x_mstride = x_mstride;
+    a.out_mstride = out_mstride;
+    a.nmembers = nmembers;
+    SW_TRY(launch_analysis(P, a, p->nwork[which], st));
+  }
+  return kOk;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* swsdc_last_error(void) { return g_last_error.c_str(); }
+const char* swsdc_version(void) { return "swsdc_b200 0.1 (sm_100a)"; }
+
+int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const double* w,
+                      swsdc_plan** out) {
+  if (!out) { set_error("out is NULL"); return kUsage; }
+  *out = nullptr;
+  if (R < 0) { set_error("truncation must be non-negative"); return kUsage; }
+  if (n_lon < 2 * R + 1) {
+    set_error("n_lon=" + std::to_string(n_lon) + " cannot carry zonal wavenumbers up to " +
+              std::to_string(R));
+    return kUsage;
+  }
+  if (n_lat < 1) { set_error("need at least one latitude"); return kUsage; }
+  if (!swfft::fft_supported(n_lon)) {
+    set_error("n_lon must factor into primes <= 13");
+    return kUsage;
+  }
+  if (!mu || !w) { set_error("mu / w are NULL"); return kUsage; }
+
+  swsdc_plan* p = new swsdc_plan();
+  PlanDev& P = p->dev;
+  P.R = R;
+  P.I = n_lon;
+  P.J = n_lat;
+  P.Jh = (n_lat + 1) / 2;
+  P.ldk = ((R + 2 + kChunk + 16) + 7) / 8 * 8;
+  P.fft = swfft::make_fft_plan(n_lon);
+  p->ldy = R + 2;
+  const int ldk = P.ldk;
+
+  std::vector<double> mu_n(P.Jh), w_n(P.Jh);
+  for (int jh = 0; jh < P.Jh; ++jh) {
+    const int jn = n_lat - P.Jh + jh;
+    mu_n[jh] = mu[jn];
+    w_n[jh] = w[jn];
+  }
+  // recurrence tables with the reference's expressions (spharm.py:159-169, 174-177)
+  std::vector<double> a((size_t)(R + 1) * ldk, 0.0), b(a.size(), 0.0), beta(a.size(), 0.0),
+      gsc(a.size(), 0.0), eps(a.size(), 0.0), sect(R + 1);
+  for (int r = 0; r <= R; ++r) {
+    double* ar = &a[(size_t)r * ldk];
+    double* br = &b[(size_t)r * ldk];
+    ar[1] = std::sqrt(2.0 * r + 3.0);
+    for (int k = 2; k < ldk; ++k) {
+      const long long s = r + k;
+      const double s2r2 = (double)(s * s - (long long)r * r);
+      ar[k] = std::sqrt((4.0 * s * s - 1.0) / s2r2);
+      br[k] = std::sqrt((2.0 * s + 1.0) * (s - 1.0 - r) * (s - 1.0 + r) / ((2.0 * s - 3.0) * s2r2));
+    }
+    double* be = &beta[(size_t)r * ldk];
+    double* g = &gsc[(size_t)r * ldk];
+    for (int k = 0; k < ldk; ++k) {
+      if (k >= 2) be[k] = br[k] / (ar[k] * ar[k - 1]);
+      g[k] = (k % kChunk == 0) ? 1.0 : g[k - 1] * ar[k];
+    }
+    double* ep = &eps[(size_t)r * ldk];
+    for (int s = r; s < ldk; ++s)
+      ep[s] = std::sqrt(((double)s * s - (double)r * r) / (4.0 * s * s - 1.0));
+    sect[r] = std::sqrt((2.0 * r + 3.0) / (2.0 * r + 2.0));
+  }
+  std::vector<int> ck_off(R + 1);
+  int nck = 0;
+  for (int r = 0; r <= R; ++r) {
+    ck_off[r] = nck;
+    nck += (R + 2 - r + kChunk - 1) / kChunk;
+  }
+  std::vector<double2> tw(n_lon);
+  for (int e = 0; e < n_lon; ++e) {
+    const long double ang = -2.0L * 3.141592653589793238462643383279502884L * e / n_lon;
+    tw[e] = make_double2((double)cosl(ang), (double)sinl(ang));
+  }
+  std::vector<int2> work[2];
+  for (int which = 0; which < 2; ++which) {
+    const int smax = R + which;
+    for (int r = 0; r <= R; ++r) {
+      const int nout = smax - r + 1;
+      for (int c = 0; c * kChunk < nout; ++c) work[which].push_back(make_int2(r, c));
+    }
+  }
+
+  int st = kOk;
+  double *d_mu = nullptr, *d_w = nullptr, *d_beta = nullptr, *d_gsc = nullptr, *d_eps = nullptr,
+         *d_a = nullptr, *d_b = nullptr, *d_sect = nullptr;
+  int* d_off = nullptr;
+  double2* d_tw = nullptr;
+  if ((st = upload(p, mu_n, &d_mu)) || (st = upload(p, w_n, &d_w)) ||
+      (st = upload(p, beta, &d_beta)) || (st = upload(p, gsc, &d_gsc)) ||
+      (st = upload(p, eps, &d_eps)) || (st = upload(p, a, &d_a)) || (st = upload(p, b, &d_b)) ||
+      (st = upload(p, sect, &d_sect)) || (st = upload(p, ck_off, &d_off)) ||
+      (st = upload(p, tw, &d_tw)) || (st = upload(p, work[0], &p->work[0])) ||
+      (st = upload(p, work[1], &p->work[1]))) {
+    swsdc_plan_destroy(p);
+    return st;
+  }
+  p->nwork[0] = (int)work[0].size();
+  p->nwork[1] = (int)work[1].size();
+  void* ck = nullptr;
+  if (cudaMalloc(&ck, sizeof(double2) * (size_t)nck * P.Jh) != cudaSuccess) {
+    set_error("cudaMalloc of the checkpoint table failed");
+    swsdc_plan_destroy(p);
+    return kCuda;
+  }
+  p->owned.push_back(ck);
+  P.mu_n = d_mu;
+  P.w_n = d_w;
+  P.beta = d_beta;
+  P.gsc = d_gsc;
+  P.eps = d_eps;
+  P.ck_off = d_off;
+  P.tw = d_tw;
+  P.ckpt = reinterpret_cast<double2*>(ck);
+  st = build_checkpoints(P, d_a, d_b, d_sect, reinterpret_cast<double2*>(ck), 0);
+  if (st == kOk && cudaDeviceSynchronize() != cudaSuccess) {
+    set_error("checkpoint build failed");
+    st = kCuda;
+  }
+  if (st != kOk) {
+    swsdc_plan_destroy(p);
+    return st;
+  }
+  *out = p;
+  return kOk;
+}
+
+int swsdc_plan_destroy(swsdc_plan* p) {
+  if (!p) return kOk;
+  cudaDeviceSynchronize();
+  for (void* ptr : p->owned) cudaFree(ptr);
+  if (p->ws) cudaFree(p->ws);
+  delete p;
+  return kOk;
+}
+
+int swsdc_plan_reserve(swsdc_plan* p, int fields) {
+  if (!p || fields < 0) { set_error("bad arguments"); return kUsage; }
+  return ensure_ws(p, fields, fields, fields);
+}
+
+int swsdc_synthesize(swsdc_plan* p, const double* coeffs, int r_in, int batch, double* grid,
+                     void* stream) {
+  if (!p) { set_error("plan is NULL"); return kUsage; }
+  if (r_in > p->dev.R) {
+    set_error("coefficients at truncation " + std::to_string(r_in) +
+              " exceed plan truncation " + std::to_string(p->dev.R));
+    return kUsage;
+  }
+  if (r_in < 0 || batch < 0) { set_error("bad truncation or batch"); return kUsage; }
+  if (batch == 0) return kOk;
+  SW_TRY(ensure_ws(p, batch, 0, 0, S(stream)));
+  const PlanDev& P = p->dev;
+  const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
+  SW_TRY(syn_plain(p, reinterpret_cast<const double2*>(coeffs), r_in, batch, ws_eo(p), S(stream)));
+  return launch_fourier_to_grid(P, ws_eo(p), fstride, grid, (long long)P.I * P.J, batch, S(stream));
+}
+
+int swsdc_analyze(swsdc_plan* p, const double* grid, int batch, double* coeffs, void* stream) {
+  if (!p) { set_error("plan is NULL"); return kUsage; }
+  if (batch < 0) { set_error("bad batch"); return kUsage; }
+  if (batch == 0) return kOk;
+  SW_TRY(ensure_ws(p, 0, batch, 0, S(stream)));
+  const PlanDev& P = p->dev;
+  const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
+  double2* x = ws_x(p, 0);
+  SW_TRY(launch_grid_to_fourier(P, 0, grid, nullptr, (long long)P.I * P.J, x, fstride, batch,
+                                S(stream)));
+  const long long plane = (long long)(P.R + 1) * (P.R + 1);
+  return ana_run(p, x, batch, 0, 1, reinterpret_cast<double2*>(coeffs), plane, P.R + 1, 0, P.R,
+                 true, S(stream));
+}
+
+int swsdc_synthesize_uv(swsdc_plan* p, const double* psi, const double* chi, int r_in, int batch,
+                        double* u, double* v, void* stream) {
+  if (!p) { set_error("plan is NULL"); return kUsage; }
+  if (r_in > p->dev.R) {
+    set_error("coefficients exceed plan truncation");
+    return kUsage;
+  }
+  if (r_in < 0 || batch < 0) { set_error("bad truncation or batch"); return kUsage; }
+  if (batch == 0) return kOk;
+  SW_TRY(ensure_ws(p, 2 * batch, 0, 0, S(stream)));
+  const PlanDev& P = p->dev;
+  const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
+  const long long cin = (long long)(r_in + 1) * (r_in + 1);
+  SynArgs a{};
+  a.src = reinterpret_cast<const double2*>(psi);
+  a.src2 = reinterpret_cast<const double2*>(chi);
+  a.src_fstride = cin;
+  a.src_R = r_in;
+  a.smax = P.R + 1;
+  a.eo = ws_eo(p);
+  a.src_mstride = cin;
+  a.eo_mstride = 2 * fstride;
+  a.nmembers = batch;
+  SW_TRY(launch_synthesis(P, a, 2, kSynUV, S(stream)));
+  const long long gstride = (long long)P.I * P.J;
+  SW_TRY(launch_fourier_to_grid(P, ws_eo(p), 2 * fstride, u, gstride, batch, S(stream)));
+  return launch_fourier_to_grid(P, ws_eo(p) + fstride, 2 * fstride, v, gstride, batch, S(stream));
+}
+
+int swsdc_analyze_divcurl(swsdc_plan* p, const double* u, const double* v, int batch, double* div,
+                          double* curl, void* stream) {
+  if (!p) { set_error("plan is NULL"); return kUsage; }
+  if (batch < 0) { set_error("bad batch"); return kUsage; }
+  if (batch == 0) return kOk;
+  SW_TRY(ensure_ws(p, 0, 4 * batch, 4 * batch, S(stream)));
+  const PlanDev& P = p->dev;
+  const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
+  double2* x = ws_x(p, 0);
+  double2* y = ws_y(p, 0, 4 * batch);
+  SW_TRY(launch_grid_to_fourier(P, 1, u, v, (long long)P.I * P.J, x, 4 * fstride, batch,
+                                S(stream)));
+  const long long yv = (long long)(P.R + 1) * p->ldy;
+  SW_TRY(ana_run(p, x, 4, 4 * fstride, batch, y, yv, p->ldy, 4 * yv, P.R + 1, false, S(stream)));
+  return launch_finalize_divcurl(P, y, 4 * yv, p->ldy, reinterpret_cast<double2*>(div),
+                                 reinterpret_cast<double2*>(curl), batch, S(stream));
+}
+
+int swsdc_eval_fe(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, const double* state,
+                  int batch, double* out, void* stream) {
+  if (!p) { set_error("plan is NULL"); return kUsage; }
+  SW_TRY(check_params(q));
+  if (batch < 0) { set_error("bad batch"); return kUsage; }
+  if (batch == 0) return kOk;
+  const bool nl = include_nonlinear != 0;
+  const int nv = nl ? 7 : 2;
+  SW_TRY(ensure_ws(p, 5 * batch, nv * batch, nv * batch, S(stream)));
+  const PlanDev& P = p->dev;
+  const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
+  const long long plane = (long long)(P.R + 1) * (P.R + 1);
+  double2* eo = ws_eo(p);
+  double2* x = ws_x(p, 5 * batch);
+  double2* y = ws_y(p, 5 * batch, nv * batch);
+  SynArgs a{};
+  a.src = reinterpret_cast<const double2*>(state);
+  a.src_fstride = plane;
+  a.src_R = P.R;
+  a.smax = P.R + 1;
+  a.radius = q->radius;
+  a.eo = eo;
+  a.src_mstride = 3 * plane;
+  a.eo_mstride = 5 * fstride;
+  a.nmembers = batch;
+  SW_TRY(launch_synthesis(P, a, 5, kSynSWE, S(stream)));
+  SW_TRY(launch_swe_grid(P, nl, eo, 5 * fstride, x, nv * fstride, batch, q->omega, q->radius,
+                         S(stream)));
+  const long long yv = (long long)(P.R + 1) * p->ldy;
+  SW_TRY(ana_run(p, x, nv, nv * fstride, batch, y, yv, p->ldy, nv * yv, P.R + 1, false,
+                 S(stream)));
+  return launch_finalize_swe(P, y, nv * yv, p->ldy, reinterpret_cast<double2*>(out), 3 * plane, nl,
+                             q->radius, batch, S(stream));
+}
+
+int swsdc_eval_fi(int R, const swsdc_params* q, const double* state, int batch, double* out,
+                  void* stream) {
+  SW_TRY(check_params(q));
+  if (R < 0 || batch < 0) { set_error("bad truncation or batch"); return kUsage; }
+  if (batch == 0) return kOk;
+  return launch_eval_fi(R, consts(q), reinterpret_cast<const double2*>(state),
+                        reinterpret_cast<double2*>(out), batch, S(stream));
+}
+
+int swsdc_solve_implicit(int R, const swsdc_params* q, double beta, const double* b, int batch,
+                         double* out, void* stream) {
+  SW_TRY(check_params(q));
+  if (beta < 0) { set_error("implicit step must be non-negative"); return kUsage; }
+  if (R < 0 || batch < 0) { set_error("bad truncation or batch"); return kUsage; }
+  const ModelConsts c = consts(q);
+  // implicit.py:330-333: the determinant depends on s only -- check on the host
+  for (int s = 0; s <= R; ++s) {
+    const double lam = (-(double)s * (s + 1.0)) / (c.radius * c.radius);
+    const double d = 1.0 - beta * c.nu * lam;
+    const double det = d * d - beta * beta * lam * c.phi_bar;
+    if (!(det > 0.0)) {
+      set_error("implicit system is singular; invalid model parameters");
+      return kNumerical;
+    }
+  }
+  if (batch == 0) return kOk;
+  return launch_solve(R, c, beta, reinterpret_cast<const double2*>(b),
+                      reinterpret_cast<double2*>(out), batch, S(stream));
+}
+
+int swsdc_combine(int n, const double* const* x, const double* w, long long count, double* out,
+                  void* stream) {
+  if (n < 0 || n > kMaxCombine || count < 0) {
+    set_error("combine takes 0..32 inputs");
+    return kUsage;
+  }
+  CombineArgs a{};
+  a.n = n;
+  a.out = out;
+  for (int k = 0; k < n; ++k) {
+    a.x[k] = x[k];
+    a.w[k] = w[k];
+  }
+  if (count == 0) return kOk;
+  return launch_combine(a, count, S(stream));
+}
+
+int swsdc_resize(const double* in, int r_in, double* out, int r_out, long long nmat, void* stream) {
+  if (r_in < 0 || r_out < 0 || nmat < 0) { set_error("bad resize arguments"); return kUsage; }
+  if (nmat == 0) return kOk;
+  return launch_resize(reinterpret_cast<const double2*>(in), r_in, reinterpret_cast<double2*>(out),
+                       r_out, nmat, S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,46 @@
+// Launch interfaces of the Legendre stage (legendre.cu).
+#pragma once
+#include "common.cuh"
+
+namespace swsdc {
+
+enum SynMode : int { kSynPlain = 0, kSynUV = 1, kSynSWE = 2 };
+
+// Output layout of synthesis: eo[b][r][jh][2] double2 = (E, O), the even- and
+// odd-degree partial sums at the north latitude of pair jh.
+struct SynArgs {
+  const double2* src;      // plain: B fields; UV: psi; SWE: state (phi, zeta, delta)
+  const double2* src2;     // UV: chi
+  long long src_fstride;   // complex elements between fields of src
+  int src_R;               // truncation of the input arrays (<= plan R; coarser inputs are zero-padded)
+  int smax;                // highest degree synthesised (R, or R+1 when H is folded onto P)
+  double radius;           // SWE: planet radius (psi = zeta / lambda, U/a, V/a)
+  double2* eo;             // output
+  long long src_mstride;   // complex elements between members (blockIdx.y)
+  long long eo_mstride;    // double2 elements between members
+  int nmembers;            // independent states / field groups in one launch
+  int nJB;                 // set by the launcher
+};
+
+// Input layout of analysis: x[v][r][jh][2] double2 = (S, D) -- the weighted
+// north+south and north-south Fourier combinations for vector v.
+struct AnaArgs {
+  const double2* x;
+  int nv;                  // number of vectors (<= 16 per launch)
+  double2* out;            // out[v * out_vstride + r * out_rstride + s]
+  long long out_vstride;
+  long long out_rstride;
+  int smax;                // highest degree written (R, or R+1 for the H shift)
+  int zero_fill;           // also write zeros for s < r
+  const int2* work;        // (r, chunk) list, one CTA each
+  long long x_mstride;     // double2 elements between members (blockIdx.y)
+  long long out_mstride;   // complex elements between members
+  int nmembers;
+};
+
+int build_checkpoints(const PlanDev& P, const double* a_tab, const double* b_tab,
+                      const double* sect_fac, double2* ckpt, cudaStream_t st);
+int launch_synthesis(const PlanDev& P, const SynArgs& a, int B, int mode, cudaStream_t st);
+int launch_analysis(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st);
+
+}  // namespace swsdc

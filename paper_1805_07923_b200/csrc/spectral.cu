@@ -1,0 +1,227 @@
+// Spectral-space kernels: O(T) per field, HBM-bound elementwise work.
+//
+//   finalize_swe      assembly of F_E from the analysed vectors incl. the
+//                     H-shift sum_j H_s y_j = (s+1) eps_s Y_{s-1} - s eps_{s+1} Y_{s+1}
+//                     and -lambda_s * analyze(KE)     (swe.py:261-279, spharm.py:171-178)
+//   finalize_divcurl  analyze_vector_div_curl assembly (spharm.py:294-300)
+//   eval_fi           L_G: gravity-wave coupling + diffusion (swe.py:206-217)
+//   solve_implicit    per-(r, s) 2x2 + scalar closed form (implicit.py:31-49)
+//   combine           sum_k w_k x_k (sdc.py:211-220, PrognosticState algebra swe.py:77-102)
+//   resize            truncate / pad (spharm.py:331-349)
+//   sweep_rhs         b = theta0 + sum_j c_j F_j + ... (sdc.py:185-202), fused
+#include "common.cuh"
+#include "spectral.cuh"
+
+namespace swsdc {
+namespace {
+
+__device__ __forceinline__ double lam_of(int s, double radius) {
+  // spharm.py:307-310  -s (s+1) / a^2
+  return (-(double)s * (s + 1.0)) / (radius * radius);
+}
+
+__device__ __forceinline__ double2 hshift(const double2* Yv, const double* eps_r, int r, int s) {
+  // (s+1) eps_s Y_{s-1} - s eps_{s+1} Y_{s+1}; eps_r == 0 so the first term is absent at s == r
+  const double2 up = Yv[s + 1];
+  const double cu = s * eps_r[s + 1];
+  double2 out = make_double2(-cu * up.x, -cu * up.y);
+  if (s > r) {
+    const double2 dn = Yv[s - 1];
+    const double cd = (s + 1.0) * eps_r[s];
+    out.x += cd * dn.x;
+    out.y += cd * dn.y;
+  }
+  return out;
+}
+
+__global__ void finalize_swe_kernel(PlanDev P, const double2* Y, long long y_mstride, int ldy,
+                                    double2* out, long long out_mstride, int nonlin,
+                                    double radius, int nmembers) {
+  const int R = P.R;
+  const long long total = (long long)nmembers * (R + 1) * (R + 1);
+  const long long plane = (long long)(R + 1) * (R + 1);
+  const long long ystride_v = (long long)(R + 1) * ldy;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(idx / plane);
+    const int rs = (int)(idx - m * plane);
+    const int r = rs / (R + 1), s = rs - r * (R + 1);
+    double2* o = out + m * out_mstride + rs;
+    double2 phi = make_double2(0.0, 0.0), zeta = phi, delta = phi;
+    if (s >= r) {
+      const double2* Ym = Y + m * y_mstride + (long long)r * ldy;
+      const double* eps_r = P.eps + (size_t)r * P.ldk;
+      if (nonlin) {
+        const double2 h0 = hshift(Ym + 4 * ystride_v, eps_r, r, s);
+        const double2 h1 = hshift(Ym + 5 * ystride_v, eps_r, r, s);
+        const double2 h2 = hshift(Ym + 6 * ystride_v, eps_r, r, s);
+        const double2 p0 = Ym[s], p1 = Ym[ystride_v + s], p2 = Ym[2 * ystride_v + s];
+        const double2 ke = Ym[3 * ystride_v + s];
+        const double lam = lam_of(s, radius);
+        phi = make_double2(p0.x + h0.x, p0.y + h0.y);
+        zeta = make_double2(p1.x + h1.x, p1.y + h1.y);
+        delta = make_double2(p2.x + h2.x - lam * ke.x, p2.y + h2.y - lam * ke.y);
+      } else {
+        zeta = Ym[s];
+        delta = Ym[ystride_v + s];
+      }
+    }
+    o[0] = phi;
+    o[plane] = zeta;
+    o[2 * plane] = delta;
+  }
+}
+
+__global__ void finalize_divcurl_kernel(PlanDev P, const double2* Y, long long y_mstride, int ldy,
+                                        double2* div, double2* curl, int nmembers) {
+  const int R = P.R;
+  const long long plane = (long long)(R + 1) * (R + 1);
+  const long long total = (long long)nmembers * plane;
+  const long long ystride_v = (long long)(R + 1) * ldy;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(idx / plane);
+    const int rs = (int)(idx - m * plane);
+    const int r = rs / (R + 1), s = rs - r * (R + 1);
+    double2 d = make_double2(0.0, 0.0), c = d;
+    if (s >= r) {
+      const double2* Ym = Y + m * y_mstride + (long long)r * ldy;
+      const double* eps_r = P.eps + (size_t)r * P.ldk;
+      const double2 hd = hshift(Ym + ystride_v, eps_r, r, s);
+      const double2 hc = hshift(Ym + 3 * ystride_v, eps_r, r, s);
+      const double2 pd = Ym[s], pc = Ym[2 * ystride_v + s];
+      d = make_double2(pd.x + hd.x, pd.y + hd.y);
+      c = make_double2(pc.x + hc.x, pc.y + hc.y);
+    }
+    div[m * plane + rs] = d;
+    curl[m * plane + rs] = c;
+  }
+}
+
+// state layout: [m][3][R+1][R+1] complex, fields (phi', zeta, delta)
+__global__ void eval_fi_kernel(int R, ModelConsts c, const double2* x, double2* out,
+                               long long nmat) {
+  const long long plane = (long long)(R + 1) * (R + 1);
+  const long long total = nmat * plane;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long m = idx / plane;
+    const int rs = (int)(idx - m * plane);
+    const int s = rs % (R + 1);
+    const double lam = lam_of(s, c.radius);
+    const double nl = c.nu * lam;
+    const double2* xm = x + m * 3 * plane + rs;
+    double2* om = out + m * 3 * plane + rs;
+    const double2 ph = xm[0], ze = xm[plane], de = xm[2 * plane];
+    om[0] = make_double2(-c.phi_bar * de.x + nl * ph.x, -c.phi_bar * de.y + nl * ph.y);
+    om[plane] = make_double2(nl * ze.x, nl * ze.y);
+    om[2 * plane] = make_double2(-lam * ph.x + nl * de.x, -lam * ph.y + nl * de.y);
+  }
+}
+
+__global__ void solve_kernel(int R, ModelConsts c, double beta, const double2* b, double2* out,
+                             long long nmat) {
+  const long long plane = (long long)(R + 1) * (R + 1);
+  const long long total = nmat * plane;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long m = idx / plane;
+    const int rs = (int)(idx - m * plane);
+    const int s = rs % (R + 1);
+    const double lam = lam_of(s, c.radius);
+    const double d = 1.0 - beta * c.nu * lam;
+    const double det = d * d - beta * beta * lam * c.phi_bar;
+    const double id = 1.0 / det;
+    const double bp = beta * c.phi_bar, bl = beta * lam;
+    const double2* bm = b + m * 3 * plane + rs;
+    double2* om = out + m * 3 * plane + rs;
+    const double2 ph = bm[0], ze = bm[plane], de = bm[2 * plane];
+    om[0] = make_double2((d * ph.x - bp * de.x) * id, (d * ph.y - bp * de.y) * id);
+    om[plane] = make_double2(ze.x / d, ze.y / d);
+    om[2 * plane] = make_double2((d * de.x - bl * ph.x) * id, (d * de.y - bl * ph.y) * id);
+  }
+}
+
+__global__ void combine_kernel(CombineArgs a, long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    if (a.n > 0) acc = a.w[0] * a.x[0][i];
+    for (int k = 1; k < a.n; ++k) acc = fma(a.w[k], a.x[k][i], acc);
+    a.out[i] = acc;
+  }
+}
+
+__global__ void resize_kernel(const double2* in, int rin, double2* out, int rout, long long nmat) {
+  const long long plane = (long long)(rout + 1) * (rout + 1);
+  const long long total = nmat * plane;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long m = idx / plane;
+    const int rs = (int)(idx - m * plane);
+    const int r = rs / (rout + 1), s = rs - r * (rout + 1);
+    double2 v = make_double2(0.0, 0.0);
+    if (r <= rin && s <= rin) v = in[m * (long long)(rin + 1) * (rin + 1) + (long long)r * (rin + 1) + s];
+    out[idx] = v;
+  }
+}
+
+int grid_for(long long n, int threads) {
+  long long b = (n + threads - 1) / threads;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+int launch_finalize_swe(const PlanDev& P, const double2* Y, long long y_mstride, int ldy,
+                        double2* out, long long out_mstride, bool nonlin, double radius,
+                        int nmembers, cudaStream_t st) {
+  const long long n = (long long)nmembers * (P.R + 1) * (P.R + 1);
+  finalize_swe_kernel<<<grid_for(n, 256), 256, 0, st>>>(P, Y, y_mstride, ldy, out, out_mstride,
+                                                        nonlin ? 1 : 0, radius, nmembers);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_finalize_divcurl(const PlanDev& P, const double2* Y, long long y_mstride, int ldy,
+                            double2* div, double2* curl, int nmembers, cudaStream_t st) {
+  const long long n = (long long)nmembers * (P.R + 1) * (P.R + 1);
+  finalize_divcurl_kernel<<<grid_for(n, 256), 256, 0, st>>>(P, Y, y_mstride, ldy, div, curl,
+                                                            nmembers);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_eval_fi(int R, const ModelConsts& c, const double2* x, double2* out, long long nmat,
+                   cudaStream_t st) {
+  const long long n = nmat * (R + 1) * (R + 1);
+  eval_fi_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, x, out, nmat);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_solve(int R, const ModelConsts& c, double beta, const double2* b, double2* out,
+                 long long nmat, cudaStream_t st) {
+  const long long n = nmat * (R + 1) * (R + 1);
+  solve_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, beta, b, out, nmat);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_combine(const CombineArgs& a, long long count, cudaStream_t st) {
+  combine_kernel<<<grid_for(count, 256), 256, 0, st>>>(a, count);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_resize(const double2* in, int rin, double2* out, int rout, long long nmat,
+                  cudaStream_t st) {
+  const long long n = nmat * (rout + 1) * (rout + 1);
+  resize_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, rin, out, rout, nmat);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+}  // namespace swsdc

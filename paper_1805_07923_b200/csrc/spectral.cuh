@@ -1,0 +1,32 @@
+// Launch interfaces of the spectral-space kernels (spectral.cu).
+#pragma once
+#include "common.cuh"
+
+namespace swsdc {
+
+struct ModelConsts {
+  double radius, omega, gravity, nu, h_bar, phi_bar;
+};
+
+constexpr int kMaxCombine = 32;
+struct CombineArgs {
+  const double* x[kMaxCombine];
+  double w[kMaxCombine];
+  double* out;
+  int n;
+};
+
+int launch_finalize_swe(const PlanDev& P, const double2* Y, long long y_mstride, int ldy,
+                        double2* out, long long out_mstride, bool nonlin, double radius,
+                        int nmembers, cudaStream_t st);
+int launch_finalize_divcurl(const PlanDev& P, const double2* Y, long long y_mstride, int ldy,
+                            double2* div, double2* curl, int nmembers, cudaStream_t st);
+int launch_eval_fi(int R, const ModelConsts& c, const double2* x, double2* out, long long nmat,
+                   cudaStream_t st);
+int launch_solve(int R, const ModelConsts& c, double beta, const double2* b, double2* out,
+                 long long nmat, cudaStream_t st);
+int launch_combine(const CombineArgs& a, long long count, cudaStream_t st);
+int launch_resize(const double2* in, int rin, double2* out, int rout, long long nmat,
+                  cudaStream_t st);
+
+}  // namespace swsdc

@@ -1,0 +1,72 @@
+"""GPU transforms vs golden vectors from the reference (tests/golden/make_golden.py)
+and vs the CPU oracle.  Tolerance: 1e-11 relative L-inf per transform
+(BASELINE.json north_star)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(os.path.join(GOLDEN, "transforms.npz"))
+
+
+def plan_for(R, I, J):
+    from paper_1805_07923_b200 import spharm
+    return spharm.TransformPlan(spharm.build_gaussian_grid(J, I), R)
+
+
+CASES = [(31, 96, 47), (31, 96, 48), (15, 48, 24), (10, 33, 17), (63, 192, 96)]
+
+
+@pytest.mark.parametrize("R,I,J", CASES)
+def test_synthesize_matches_reference(golden, R, I, J):
+    tag = f"R{R}_I{I}_J{J}"
+    plan = plan_for(R, I, J)
+    got = plan.synthesize(golden[f"{tag}_c"])
+    assert rel_err(got, golden[f"{tag}_syn"]) < TOL
+
+
+@pytest.mark.parametrize("R,I,J", CASES)
+def test_analyze_matches_reference(golden, R, I, J):
+    tag = f"R{R}_I{I}_J{J}"
+    plan = plan_for(R, I, J)
+    got = plan.analyze(golden[f"{tag}_g"])
+    assert rel_err(got, golden[f"{tag}_ana"]) < TOL
+
+
+@pytest.mark.parametrize("R,I,J", CASES)
+def test_vector_transforms_match_reference(golden, R, I, J):
+    tag = f"R{R}_I{I}_J{J}"
+    plan = plan_for(R, I, J)
+    u, v = plan.synthesize_pair_cos_gradient(golden[f"{tag}_c"], golden[f"{tag}_c2"])
+    assert rel_err(u, golden[f"{tag}_u"]) < TOL
+    assert rel_err(v, golden[f"{tag}_v"]) < TOL
+    d, k = plan.analyze_vector_div_curl(golden[f"{tag}_g"], golden[f"{tag}_g2"])
+    assert rel_err(d, golden[f"{tag}_div"]) < TOL
+    assert rel_err(k, golden[f"{tag}_curl"]) < TOL
+
+
+def test_batched_transforms_match_oracle():
+    import swsdc_oracle as orc
+    from paper_1805_07923_b200 import workloads
+    R, I, J = 63, 192, 96
+    plan = plan_for(R, I, J)
+    oplan = orc.OraclePlan(R, I, J)
+    c = workloads.transform_batch(R, 15)
+    g = plan.synthesize(torch.as_tensor(c).cuda())
+    want = np.stack([oplan.synthesize(ci) for ci in c])
+    assert rel_err(g.cpu().numpy(), want) < TOL
+    back = plan.analyze(g)
+    want_b = np.stack([oplan.analyze(gi) for gi in want])
+    assert rel_err(back.cpu().numpy(), want_b) < TOL
+    assert rel_err(back.cpu().numpy(), c) < TOL
