@@ -1,0 +1,409 @@
+"""Benchmark of the B200 MLSDC-SH hot path (driver contract).
+
+Headline (BASELINE.json configs[1]): SH transform-pair throughput at T255 on the
+384x768 Gaussian grid, fp64, batch of 15 seeded fields (3 variables x 5 nodes);
+one step = synthesize + analyze of the batch, inputs resident in HBM, L2 flushed
+(256 MiB write) before every timed step.  `e2e` is the same metric through the
+public API with pinned HOST buffers, H2D of the coefficients and D2H of the
+result inside every timed step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun, one rank per GPU): every rank transforms its own batch
+(weak scaling, no data-path collective); value = fields of all ranks / max time.
+`--impl reference` times the CPU oracle port (oracle/swsdc_oracle.py, a numpy
+restatement of the reference's own dense-table algorithm) on the host cores,
+rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+R, I, J, NF = 255, 768, 384, 15
+WORKLOAD = "config1: SH transform pair (synthesize+analyze), T255 on 384x768 Gaussian grid, fp64, 15 fields"
+METRIC = "SH transform pairs/s (fp64)"
+UNIT = "field-pairs/s"
+FP64_FALLBACK_TFLOPS = 36.9   # profiles/fp64_peak_r01.txt (tools/fp64_peak.cu on B200)
+
+
+# ----------------------------------------------------------------------------
+# algorithmic work per field
+# ----------------------------------------------------------------------------
+def legendre_flops(Rr, Jj):
+    T = (Rr + 1) * (Rr + 2) // 2
+    return 2.0 * T * Jj                        # per field per direction
+
+
+def fft_flops(Ii, Jj):
+    return 2.5 * Ii * math.log2(Ii) * Jj       # per field per direction
+
+
+def grid_bytes(Ii, Jj):
+    return 8.0 * Ii * Jj
+
+
+def coeff_bytes(Rr):
+    return 16.0 * (Rr + 1) * (Rr + 2) / 2      # triangular complex128
+
+
+# ----------------------------------------------------------------------------
+# distributed plumbing
+# ----------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def init_dist(world, backend):
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend=backend)
+    return dist if world > 1 else None
+
+
+def max_over_ranks(x, dist, device):
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------
+# clocks during the timed region (NVML sampler thread)
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index, period=0.005):
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self.period = period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv is not None:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        reasons = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples), "reasons": reasons}
+
+
+# ----------------------------------------------------------------------------
+# CPU baseline: the oracle port (numpy, reference dense-table algorithm)
+# ----------------------------------------------------------------------------
+_PLAN = None
+
+
+def _cpu_init():
+    """Pool initializer: one dense-table oracle plan per worker (plan build is
+    setup, excluded from timing as in the reference harness, harness.py:234)."""
+    global _PLAN
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import swsdc_oracle as orc
+    _PLAN = orc.OraclePlan(R, I, J)
+
+
+def _cpu_pair(idx):
+    from paper_1805_07923_b200 import workloads
+    c = workloads.spectral_noise(np.random.default_rng(idx), R, workloads.RMS_TARGETS[idx % 3],
+                                 idx % 3 != 0)
+    t0 = time.perf_counter()
+    g = _PLAN.synthesize(c)
+    c2 = _PLAN.analyze(g)
+    return time.perf_counter() - t0, float(np.max(np.abs(c2 - c)) / np.max(np.abs(c)))
+
+
+class CpuPool:
+    """Single-threaded oracle workers (OPENBLAS_NUM_THREADS=1, the reference's
+    fastest setting per SURVEY §3), one per core."""
+
+    def __init__(self, n_workers):
+        import multiprocessing as mp
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"   # inherited by the spawned workers
+        self.n = n_workers
+        self.pool = mp.get_context("spawn").Pool(n_workers, initializer=_cpu_init)
+        self.pool.map(_cpu_pair, range(n_workers), chunksize=1)   # warm
+
+    def step(self, nfields):
+        """Wall time of one batch of `nfields` field pairs over the pool."""
+        t0 = time.perf_counter()
+        res = self.pool.map(_cpu_pair, range(nfields), chunksize=1)
+        return time.perf_counter() - t0, max(e for _, e in res)
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle port on all host cores, rank 0 only."""
+    if rank != 0:
+        return
+    workers = max(1, min(host_cores(), NF))
+    pool = CpuPool(workers)
+    for _ in range(args.warmup):
+        pool.step(NF)
+    t_steps = [pool.step(NF)[0] for _ in range(args.steps)]
+    pool.close()
+    value = NF * len(t_steps) / sum(t_steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(t_steps) / len(t_steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded spectra, SURVEY §8d)",
+        "config": {"workload": WORKLOAD, "R": R, "grid": [I, J], "fields": NF},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": f"each step: {NF} field pairs over {workers} single-threaded "
+                                   f"workers (oracle/swsdc_oracle.py: reference dense tables + "
+                                   f"pocketfft, OPENBLAS_NUM_THREADS=1)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_1805_07923_b200 import _lib, spharm, workloads
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = init_dist(world, "nccl")
+
+    plan = spharm.TransformPlan(spharm.build_gaussian_grid(J, I), R, device=dev)
+    plan.reserve(NF)
+    c_host = workloads.transform_batch(R, NF)
+    c = torch.as_tensor(c_host, device=dev)
+    g = torch.empty((NF, I, J), dtype=torch.float64, device=dev)
+    out = torch.empty_like(c)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def step():
+        plan.synthesize(c, out=g)
+        plan.analyze(g, out=out)
+
+    # warm-up + correctness of this very batch (round trip of band-limited input)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    rt_err = float((out - c).abs().max() / c.abs().max())
+
+    peak_fp64 = _lib.probe_fp64(20)
+    peak_src = "measured live: swsdc_probe_fp64 (DFMA, 148x16 CTAs)"
+    if not (peak_fp64 > 1.0):
+        peak_fp64, peak_src = FP64_FALLBACK_TFLOPS, "profiles/fp64_peak_r01.txt"
+
+    # soak so the clock sampler sees a loaded GPU, then the timed region
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        t_soak = time.perf_counter()
+        while time.perf_counter() - t_soak < args.soak:
+            for _ in range(20):
+                step()
+            torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = _lib.launch_count()
+        _lib.profile_enable(True)
+        for k in range(args.steps):
+            flush.zero_()
+            starts[k].record()
+            step()
+            ends[k].record()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        launches = _lib.launch_count() - l0
+        stages = _lib.profile_collect()
+        _lib.profile_enable(False)
+    t_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    t_ms = max_over_ranks(t_ms, dist, dev)
+    value = world * NF * args.steps / (t_ms * 1e-3)
+
+    # e2e through the public API with pinned host buffers
+    c_pin = torch.from_numpy(c_host).pin_memory()
+    o_pin = torch.empty_like(c_pin).pin_memory()
+    c_dev = torch.empty_like(c)
+
+    def step_e2e():
+        c_dev.copy_(c_pin, non_blocking=True)
+        plan.synthesize(c_dev, out=g)
+        plan.analyze(g, out=out)
+        o_pin.copy_(out, non_blocking=True)
+
+    for _ in range(3):
+        step_e2e()
+    torch.cuda.synchronize()
+    e_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    for k in range(args.steps):
+        flush.zero_()
+        e_s[k].record()
+        step_e2e()
+        e_e[k].record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(sum(s.elapsed_time(e) for s, e in zip(e_s, e_e)), dist, dev)
+    e2e_value = world * NF * args.steps / (e2e_ms * 1e-3)
+    e2e_err = float(np.max(np.abs(o_pin.numpy() - c_host)) / np.max(np.abs(c_host)))
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant stage
+    per_launch_flops = {
+        "legendre_synthesis": NF * legendre_flops(R, J),
+        "legendre_analysis": NF * legendre_flops(R, J),
+        "fourier_to_grid": NF * fft_flops(I, J),
+        "grid_to_fourier": NF * fft_flops(I, J),
+    }
+    per_launch_bytes = {
+        "fourier_to_grid": NF * grid_bytes(I, J),
+        "grid_to_fourier": NF * grid_bytes(I, J),
+        "legendre_synthesis": NF * coeff_bytes(R),
+        "legendre_analysis": NF * coeff_bytes(R),
+    }
+    stage_ms = {k: v[1] / max(v[0], 1) for k, v in stages.items()}
+    dom = max(stages, key=lambda k: stages[k][1])
+    dom_ms = stage_ms[dom]
+    hbm_peak = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm_peak = json.load(f).get("hbm_gbs")
+    except Exception:
+        pass
+    if dom.startswith("legendre"):
+        achieved = per_launch_flops[dom] / (dom_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
+                "frac": achieved / peak_fp64, "traffic": None, "kernel": dom,
+                "peak_kind": "fp64 FMA pipe (DFMA == DMMA on sm_100a)", "peak_source": peak_src,
+                "work": f"{NF} fields x 2*T*J flops, T=(R+1)(R+2)/2"}
+    else:
+        hb = hbm_peak or 6547.2
+        achieved = per_launch_bytes[dom] / (dom_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hb, "unit": "GB/s",
+                "frac": achieved / hb, "traffic": None, "kernel": dom,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
+    pair_flops = NF * 2 * (legendre_flops(R, J) + fft_flops(I, J))
+    step_s = t_ms * 1e-3 / args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded spectra, amplitude (n+1)^-1.5, rms 1e3/1e-5/1e-6; SURVEY §8d)",
+        "config": {"workload": WORKLOAD, "R": R, "grid": [I, J], "fields": NF,
+                   "global_fields": NF * world, "parallelism": f"replicas x{world} (weak)",
+                   "l2": "flushed (256 MiB write) before every timed step"},
+        "roofline": roof,
+        "step_roofline": {"flops": pair_flops, "achieved_tflops": pair_flops / step_s / 1e12,
+                          "frac_fp64": pair_flops / step_s / 1e12 / peak_fp64},
+        "stages_ms_per_launch": stage_ms,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(c_pin.numel() * 16),
+                "d2h_bytes_per_step": int(o_pin.numel() * 16), "ms_per_step": e2e_ms / args.steps,
+                "roundtrip_err": e2e_err},
+        "roundtrip_err": rt_err,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        workers = max(1, min(host_cores(), NF))
+        pool = CpuPool(workers)
+        ts = [pool.step(NF)[0] for _ in range(3)]
+        pool.close()
+        one = CpuPool(1)
+        t1 = one.step(3)[0]
+        one.close()
+        rate = NF * len(ts) / sum(ts)
+        line["cpu_baseline"] = {
+            "value": rate, "unit": UNIT, "cores": workers, "kind": "port",
+            "sample": f"3 batches of {NF} T255 field pairs over {workers} single-threaded oracle "
+                      f"workers (plan build excluded); 1 core: {3 / t1:.2f} {UNIT}"}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--soak", type=float, default=1.0, help="seconds of load before timing")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -83,6 +83,16 @@ int swsdc_combine(int n, const double* const* x, const double* w, long long coun
 /* spharm.truncate / spharm.pad (spharm.py:331-349) over `nmat` (R+1)^2 matrices. */
 int swsdc_resize(const double* in, int r_in, double* out, int r_out, long long nmat, void* stream);
 
+/* Launch accounting / stage timing (bench.py): number of kernels launched by
+ * this library so far; per-stage CUDA-event timing on/off (clears records);
+ * collect "stage<TAB>launches<TAB>total_ms" lines, returns bytes needed. */
+long long swsdc_launch_count(void);
+int swsdc_profile_enable(int on);
+int swsdc_profile_collect(char* buf, int buflen);
+/* FP64 FMA throughput probe (TFLOP/s) on the current device: the roofline
+ * denominator bench.py measures live. */
+int swsdc_probe_fp64(int reps, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

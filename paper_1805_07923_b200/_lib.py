@@ -46,6 +46,10 @@ _SIGNATURES = {
     "swsdc_solve_implicit": ([_I, ctypes.POINTER(Params), _D, _P, _I, _P, _P], _I),
     "swsdc_combine": ([_I, ctypes.POINTER(_P), ctypes.POINTER(_D), _LL, _P, _P], _I),
     "swsdc_resize": ([_P, _I, _P, _I, _LL, _P], _I),
+    "swsdc_launch_count": ([], _LL),
+    "swsdc_profile_enable": ([_I], _I),
+    "swsdc_profile_collect": ([ctypes.c_char_p, _I], _I),
+    "swsdc_probe_fp64": ([_I, ctypes.POINTER(_D)], _I),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
@@ -83,3 +87,31 @@ def check(status: int) -> None:
 
 def params_struct(p) -> Params:
     return Params(p.radius, p.omega, p.gravity, p.nu, p.h_bar)
+
+
+def launch_count() -> int:
+    return int(load().swsdc_launch_count())
+
+
+def profile_enable(on: bool) -> None:
+    load().swsdc_profile_enable(1 if on else 0)
+
+
+def profile_collect() -> dict:
+    """{stage: (launches, total_ms)} of the events recorded since profile_enable."""
+    lib = load()
+    need = lib.swsdc_profile_collect(None, 0)
+    buf = ctypes.create_string_buffer(max(need, 1))
+    lib.swsdc_profile_collect(buf, len(buf))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, n, ms = line.split("\t")
+        out[name] = (int(n), float(ms))
+    return out
+
+
+def probe_fp64(reps: int = 20) -> float:
+    """Measured FP64 FMA peak of the current device, TFLOP/s."""
+    out = ctypes.c_double()
+    check(load().swsdc_probe_fp64(reps, ctypes.byref(out)))
+    return float(out.value)

@@ -42,6 +42,20 @@ void set_error(const std::string& msg);
     if (_s != ::swsdc::kOk) return _s;    \
   } while (0)
 
+// RAII bracket of one kernel launch: counts it and, when profiling is on,
+// records CUDA events around it on `st` (profile.cu).
+class StageScope {
+ public:
+  StageScope(const char* name, cudaStream_t st);
+  ~StageScope();
+  StageScope(const StageScope&) = delete;
+  StageScope& operator=(const StageScope&) = delete;
+
+ private:
+  int idx_;
+  cudaStream_t st_;
+};
+
 // Read-only device view of one transform plan (passed by value to kernels).
 //
 // Latitude indexing: jh in [0, Jh), Jh = ceil(J/2).  The "north" latitude of

@@ -310,6 +310,7 @@ int f2g_launch(const PlanDev& P, const double2* eo, long long eo_fstride, double
   const size_t smem = sizeof(double2) * np * P.I;
   SW_TRY(set_smem((const void*)f2g_kernel<BIGP>, smem));
   dim3 gridDim((P.Jh + np - 1) / np, nf);
+  StageScope sc("fourier_to_grid", st);
   f2g_kernel<BIGP><<<gridDim, pick_threads(np * P.I / 4, BIGP), smem, st>>>(P, eo, eo_fstride, grid,
                                                                        grid_fstride, np);
   SW_LAUNCH_CHECK();
@@ -324,6 +325,7 @@ int g2f_launch(const PlanDev& P, const double* grid, const double* grid2, long l
   const size_t smem = sizeof(double2) * nin * np * P.I;
   dim3 gridDim((P.Jh + np - 1) / np, nf);
   SW_TRY(set_smem((const void*)g2f_kernel<MODE, BIGP>, smem));
+  StageScope sc(MODE == 0 ? "grid_to_fourier" : "grid_to_fourier_divcurl", st);
   g2f_kernel<MODE, BIGP><<<gridDim, pick_threads(nin * np * P.I / 4, BIGP), smem, st>>>(
       P, grid, grid2, grid_fstride, x, x_fstride, np);
   SW_LAUNCH_CHECK();
@@ -337,6 +339,7 @@ int swe_launch(const PlanDev& P, const double2* eo, long long eo_mstride, double
   const size_t smem = sizeof(double2) * nr * P.I;
   dim3 gridDim(P.Jh, nmembers);
   SW_TRY(set_smem((const void*)swe_grid_kernel<NONLIN, BIGP>, smem));
+  StageScope sc("swe_grid", st);
   swe_grid_kernel<NONLIN, BIGP><<<gridDim, pick_threads(nr * P.I / 4, BIGP), smem, st>>>(
       P, eo, eo_mstride, x, x_mstride, omega, radius);
   SW_LAUNCH_CHECK();

@@ -66,6 +66,7 @@ __global__ void build_checkpoints_kernel(PlanDev P, const double* a_tab, const d
 int build_checkpoints(const PlanDev& P, const double* a_tab, const double* b_tab,
                       const double* sect_fac, double2* ckpt, cudaStream_t st) {
   const int threads = 64;
+  StageScope sc("build_checkpoints", st);
   build_checkpoints_kernel<<<(P.Jh + threads - 1) / threads, threads, 0, st>>>(P, a_tab, b_tab,
                                                                                sect_fac, ckpt);
   SW_LAUNCH_CHECK();
@@ -267,6 +268,7 @@ int launch_syn_t(const PlanDev& P, const SynArgs& a0, cudaStream_t st) {
                       sizeof(double2) * 2 * B * kSynLat;
   auto kern = syn_kernel<B, MODE>;
   if (smem > 48 * 1024) SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  StageScope sc("legendre_synthesis", st);
   kern<<<dim3((P.R + 1) * a.nJB, a.nmembers), kSynWarps * 32, smem, st>>>(P, a);
   SW_LAUNCH_CHECK();
   return kOk;
@@ -414,6 +416,7 @@ int launch_ana_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st)
   const size_t smem = sizeof(double) * (32 * kAnaQS + 2 * kAnaJC * XS + kChunk);
   auto kern = ana_kernel<NT>;
   if (smem > 48 * 1024) SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  StageScope sc("legendre_analysis", st);
   kern<<<dim3(nwork, a.nmembers), kAnaThreads, smem, st>>>(P, a);
   SW_LAUNCH_CHECK();
   return kOk;

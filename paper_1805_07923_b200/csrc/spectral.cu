@@ -179,6 +179,7 @@ int launch_finalize_swe(const PlanDev& P, const double2* Y, long long y_mstride,
                         double2* out, long long out_mstride, bool nonlin, double radius,
                         int nmembers, cudaStream_t st) {
   const long long n = (long long)nmembers * (P.R + 1) * (P.R + 1);
+  StageScope sc("finalize_swe", st);
   finalize_swe_kernel<<<grid_for(n, 256), 256, 0, st>>>(P, Y, y_mstride, ldy, out, out_mstride,
                                                         nonlin ? 1 : 0, radius, nmembers);
   SW_LAUNCH_CHECK();
@@ -188,6 +189,7 @@ int launch_finalize_swe(const PlanDev& P, const double2* Y, long long y_mstride,
 int launch_finalize_divcurl(const PlanDev& P, const double2* Y, long long y_mstride, int ldy,
                             double2* div, double2* curl, int nmembers, cudaStream_t st) {
   const long long n = (long long)nmembers * (P.R + 1) * (P.R + 1);
+  StageScope sc("finalize_divcurl", st);
   finalize_divcurl_kernel<<<grid_for(n, 256), 256, 0, st>>>(P, Y, y_mstride, ldy, div, curl,
                                                             nmembers);
   SW_LAUNCH_CHECK();
@@ -197,6 +199,7 @@ int launch_finalize_divcurl(const PlanDev& P, const double2* Y, long long y_mstr
 int launch_eval_fi(int R, const ModelConsts& c, const double2* x, double2* out, long long nmat,
                    cudaStream_t st) {
   const long long n = nmat * (R + 1) * (R + 1);
+  StageScope sc("eval_fi", st);
   eval_fi_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, x, out, nmat);
   SW_LAUNCH_CHECK();
   return kOk;
@@ -205,12 +208,14 @@ int launch_eval_fi(int R, const ModelConsts& c, const double2* x, double2* out, 
 int launch_solve(int R, const ModelConsts& c, double beta, const double2* b, double2* out,
                  long long nmat, cudaStream_t st) {
   const long long n = nmat * (R + 1) * (R + 1);
+  StageScope sc("solve_implicit", st);
   solve_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, beta, b, out, nmat);
   SW_LAUNCH_CHECK();
   return kOk;
 }
 
 int launch_combine(const CombineArgs& a, long long count, cudaStream_t st) {
+  StageScope sc("combine", st);
   combine_kernel<<<grid_for(count, 256), 256, 0, st>>>(a, count);
   SW_LAUNCH_CHECK();
   return kOk;
@@ -219,6 +224,7 @@ int launch_combine(const CombineArgs& a, long long count, cudaStream_t st) {
 int launch_resize(const double2* in, int rin, double2* out, int rout, long long nmat,
                   cudaStream_t st) {
   const long long n = nmat * (rout + 1) * (rout + 1);
+  StageScope sc("resize", st);
   resize_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, rin, out, rout, nmat);
   SW_LAUNCH_CHECK();
   return kOk;

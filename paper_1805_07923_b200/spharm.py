@@ -233,25 +233,33 @@ class TransformPlan:
         return t, host, r_in
 
     # -- public transforms (spharm.py:254-300) ------------------------------
-    def analyze(self, field):
-        """Grid field (..., n_lon, n_lat) -> coefficients (..., R+1, R+1)."""
+    def analyze(self, field, out: torch.Tensor | None = None):
+        """Grid field (..., n_lon, n_lat) -> coefficients (..., R+1, R+1).
+        `out` (optional, CUDA, contiguous) receives the result in place."""
         g, host = self._grid_in(field)
         lead = g.shape[:-2]
         nb = int(np.prod(lead)) if lead else 1
         R = self.truncation
-        out = torch.empty(lead + (R + 1, R + 1), dtype=torch.complex128, device=self.device)
+        if out is None:
+            out = torch.empty(lead + (R + 1, R + 1), dtype=torch.complex128, device=self.device)
+        elif tuple(out.shape) != tuple(lead) + (R + 1, R + 1) or not out.is_contiguous():
+            raise ValueError("out has the wrong shape or layout")
         with torch.cuda.device(self.device):
             _lib.check(self._lib.swsdc_analyze(self._handle, _ptr(g), nb, _ptr(out),
                                                _stream_ptr(self.device)))
         return _out(out, host)
 
-    def synthesize(self, coeffs):
-        """Coefficients (..., R_in+1, R_in+1), R_in <= R -> real grid (..., n_lon, n_lat)."""
+    def synthesize(self, coeffs, out: torch.Tensor | None = None):
+        """Coefficients (..., R_in+1, R_in+1), R_in <= R -> real grid (..., n_lon, n_lat).
+        `out` (optional, CUDA, contiguous) receives the result in place."""
         c, host, r_in = self._coeff_in(coeffs)
         lead = c.shape[:-2]
         nb = int(np.prod(lead)) if lead else 1
-        out = torch.empty(lead + (self.grid.n_lon, self.grid.n_lat), dtype=torch.float64,
-                          device=self.device)
+        shape = tuple(lead) + (self.grid.n_lon, self.grid.n_lat)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.float64, device=self.device)
+        elif tuple(out.shape) != shape or not out.is_contiguous():
+            raise ValueError("out has the wrong shape or layout")
         with torch.cuda.device(self.device):
             _lib.check(self._lib.swsdc_synthesize(self._handle, _ptr(c), r_in, nb, _ptr(out),
                                                   _stream_ptr(self.device)))
