@@ -52,8 +52,14 @@ size_t y_bytes(const swsdc_plan* p) {
   return (size_t)(p->dev.R + 1) * p->ldy * sizeof(double2);
 }
 
-int ensure_ws(swsdc_plan* p, int n_eo, int n_x, int n_y, cudaStream_t st = 0) {
-  const size_t need = (size_t)(n_eo + n_x) * field_bytes(p) + (size_t)n_y * y_bytes(p) + 256;
+// Workspace = [eo: n_eo fields][x: x_bytes][y: n_y vectors].
+size_t x_bytes_for(const swsdc_plan* p, int nv, int nmembers) {
+  if (nv <= 0 || nmembers <= 0) return 0;
+  return sizeof(double) * (size_t)make_xlayout(p->dev.R, p->dev.Jh, nv).mstride * nmembers + 256;
+}
+
+int ensure_ws(swsdc_plan* p, int n_eo, size_t x_bytes, int n_y, cudaStream_t st = 0) {
+  const size_t need = (size_t)n_eo * field_bytes(p) + x_bytes + (size_t)n_y * y_bytes(p) + 256;
   if (need <= p->ws_bytes) return kOk;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   // growing the workspace cannot happen during graph capture
@@ -73,11 +79,11 @@ int ensure_ws(swsdc_plan* p, int n_eo, int n_x, int n_y, cudaStream_t st = 0) {
 }
 
 double2* ws_eo(swsdc_plan* p) { return reinterpret_cast<double2*>(p->ws); }
-double2* ws_x(swsdc_plan* p, int n_eo) {
-  return reinterpret_cast<double2*>(p->ws + (size_t)n_eo * field_bytes(p));
+double* ws_x(swsdc_plan* p, int n_eo) {
+  return reinterpret_cast<double*>(p->ws + (size_t)n_eo * field_bytes(p));
 }
-double2* ws_y(swsdc_plan* p, int n_eo, int n_x) {
-  return reinterpret_cast<double2*>(p->ws + (size_t)(n_eo + n_x) * field_bytes(p));
+double2* ws_y(swsdc_plan* p, int n_eo, size_t x_bytes) {
+  return reinterpret_cast<double2*>(p->ws + (size_t)n_eo * field_bytes(p) + x_bytes);
 }
 
 ModelConsts consts(const swsdc_params* q) {
@@ -108,14 +114,14 @@ int syn_plain(swsdc_plan* p, const double2* coeffs, int r_in, int batch, double2
   const long long cin = (long long)(r_in + 1) * (r_in + 1);
   const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
   int B = 0;
-  for (int cand = 8; cand >= 4; --cand)
+  for (int cand = 6; cand >= 4; --cand)
     if (batch % cand == 0) { B = cand; break; }
   int done = 0;
   while (done < batch) {
     int b = B;
     int groups;
     if (b == 0) {
-      const int ng = (batch - done + 7) / 8;
+      const int ng = (batch - done + 5) / 6;
       b = (batch - done + ng - 1) / ng;
     }
     groups = (batch - done) / b;
@@ -135,24 +141,23 @@ int syn_plain(swsdc_plan* p, const double2* coeffs, int r_in, int batch, double2
   return kOk;
 }
 
-// Legendre analysis of nv vectors per member into out (dense or Y scratch).
-int ana_run(swsdc_plan* p, const double2* x, int nv, long long x_mstride, int nmembers,
-            double2* out, long long out_vstride, long long out_rstride, long long out_mstride,
-            int smax, bool zero_fill, cudaStream_t st) {
+// Legendre analysis of the nv vectors (XLayout xl) of each member into out.
+int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, double2* out,
+            long long out_vstride, long long out_rstride, long long out_mstride, int smax,
+            bool zero_fill, cudaStream_t st) {
   const PlanDev& P = p->dev;
   const int which = (smax == P.R) ? 0 : 1;
-  const long long vstride_x = (long long)(P.R + 1) * P.Jh * 2;
-  for (int v0 = 0; v0 < nv; v0 += 16) {
+  for (int v0 = 0; v0 < xl.nv; v0 += 16) {
     AnaArgs a{};
-    a.nv = (nv - v0 < 16) ? nv - v0 : 16;
-    a.x = x + v0 * vstride_x;
+    a.nv = (xl.nv - v0 < 16) ? xl.nv - v0 : 16;
+    a.x = x + (size_t)(v0 / 16) * xl.gstride;
+    a.xl = xl;
     a.out = out + v0 * out_vstride;
     a.out_vstride = out_vstride;
     a.out_rstride = out_rstride;
     a.smax = smax;
     a.zero_fill = zero_fill ? 1 : 0;
     a.work = p->work[which];
-    a.x_mstride = x_mstride;
     a.out_mstride = out_mstride;
     a.nmembers = nmembers;
     SW_TRY(launch_analysis(P, a, p->nwork[which], st));
@@ -236,12 +241,20 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
     const long double ang = -2.0L * 3.141592653589793238462643383279502884L * e / n_lon;
     tw[e] = make_double2((double)cosl(ang), (double)sinl(ang));
   }
+  std::vector<int> rev(n_lon);
+  for (int k = 0; k < n_lon; ++k) rev[k] = swfft::pad_idx(swfft::digit_rev(P.fft, k));
+  {
+    int rs = swfft::padded_len(n_lon);
+    rs += (9 - rs % 8) % 8;  // == 1 (mod 8) double2 slots: rings differ in bank group
+    P.ring_stride = rs;
+  }
   std::vector<int2> work[2];
   for (int which = 0; which < 2; ++which) {
     const int smax = R + which;
     for (int r = 0; r <= R; ++r) {
       const int nout = smax - r + 1;
-      for (int c = 0; c * kChunk < nout; ++c) work[which].push_back(make_int2(r, c));
+      const int wpc = ana_warps_per_cta();
+      for (int c = 0; c * kChunk < nout; c += wpc) work[which].push_back(make_int2(r, c));
     }
   }
 
@@ -249,12 +262,13 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
   double *d_mu = nullptr, *d_w = nullptr, *d_beta = nullptr, *d_gsc = nullptr, *d_eps = nullptr,
          *d_a = nullptr, *d_b = nullptr, *d_sect = nullptr;
   int* d_off = nullptr;
+  int* d_rev = nullptr;
   double2* d_tw = nullptr;
   if ((st = upload(p, mu_n, &d_mu)) || (st = upload(p, w_n, &d_w)) ||
       (st = upload(p, beta, &d_beta)) || (st = upload(p, gsc, &d_gsc)) ||
       (st = upload(p, eps, &d_eps)) || (st = upload(p, a, &d_a)) || (st = upload(p, b, &d_b)) ||
       (st = upload(p, sect, &d_sect)) || (st = upload(p, ck_off, &d_off)) ||
-      (st = upload(p, tw, &d_tw)) || (st = upload(p, work[0], &p->work[0])) ||
+      (st = upload(p, tw, &d_tw)) || (st = upload(p, rev, &d_rev)) || (st = upload(p, work[0], &p->work[0])) ||
       (st = upload(p, work[1], &p->work[1]))) {
     swsdc_plan_destroy(p);
     return st;
@@ -275,6 +289,7 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
   P.eps = d_eps;
   P.ck_off = d_off;
   P.tw = d_tw;
+  P.rev = d_rev;
   P.ckpt = reinterpret_cast<double2*>(ck);
   st = build_checkpoints(P, d_a, d_b, d_sect, reinterpret_cast<double2*>(ck), 0);
   if (st == kOk && cudaDeviceSynchronize() != cudaSuccess) {
@@ -300,7 +315,8 @@ int swsdc_plan_destroy(swsdc_plan* p) {
 
 int swsdc_plan_reserve(swsdc_plan* p, int fields) {
   if (!p || fields < 0) { set_error("bad arguments"); return kUsage; }
-  return ensure_ws(p, fields, fields, fields);
+  return ensure_ws(p, 5 * fields, x_bytes_for(p, 7, fields) + x_bytes_for(p, fields, 1),
+                   7 * fields);
 }
 
 int swsdc_synthesize(swsdc_plan* p, const double* coeffs, int r_in, int batch, double* grid,
@@ -324,15 +340,15 @@ int swsdc_analyze(swsdc_plan* p, const double* grid, int batch, double* coeffs, 
   if (!p) { set_error("plan is NULL"); return kUsage; }
   if (batch < 0) { set_error("bad batch"); return kUsage; }
   if (batch == 0) return kOk;
-  SW_TRY(ensure_ws(p, 0, batch, 0, S(stream)));
+  SW_TRY(ensure_ws(p, 0, x_bytes_for(p, batch, 1), 0, S(stream)));
   const PlanDev& P = p->dev;
-  const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
-  double2* x = ws_x(p, 0);
-  SW_TRY(launch_grid_to_fourier(P, 0, grid, nullptr, (long long)P.I * P.J, x, fstride, batch,
+  const XLayout xl = make_xlayout(P.R, P.Jh, batch);
+  double* x = ws_x(p, 0);
+  SW_TRY(launch_grid_to_fourier(P, 0, grid, nullptr, (long long)P.I * P.J, x, xl, batch,
                                 S(stream)));
   const long long plane = (long long)(P.R + 1) * (P.R + 1);
-  return ana_run(p, x, batch, 0, 1, reinterpret_cast<double2*>(coeffs), plane, P.R + 1, 0, P.R,
-                 true, S(stream));
+  return ana_run(p, x, xl, 1, reinterpret_cast<double2*>(coeffs), plane, P.R + 1, 0, P.R, true,
+                 S(stream));
 }
 
 int swsdc_synthesize_uv(swsdc_plan* p, const double* psi, const double* chi, int r_in, int batch,
@@ -369,15 +385,15 @@ int swsdc_analyze_divcurl(swsdc_plan* p, const double* u, const double* v, int b
   if (!p) { set_error("plan is NULL"); return kUsage; }
   if (batch < 0) { set_error("bad batch"); return kUsage; }
   if (batch == 0) return kOk;
-  SW_TRY(ensure_ws(p, 0, 4 * batch, 4 * batch, S(stream)));
+  const size_t xb = x_bytes_for(p, 4, batch);
+  SW_TRY(ensure_ws(p, 0, xb, 4 * batch, S(stream)));
   const PlanDev& P = p->dev;
-  const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
-  double2* x = ws_x(p, 0);
-  double2* y = ws_y(p, 0, 4 * batch);
-  SW_TRY(launch_grid_to_fourier(P, 1, u, v, (long long)P.I * P.J, x, 4 * fstride, batch,
-                                S(stream)));
+  const XLayout xl = make_xlayout(P.R, P.Jh, 4);
+  double* x = ws_x(p, 0);
+  double2* y = ws_y(p, 0, xb);
+  SW_TRY(launch_grid_to_fourier(P, 1, u, v, (long long)P.I * P.J, x, xl, batch, S(stream)));
   const long long yv = (long long)(P.R + 1) * p->ldy;
-  SW_TRY(ana_run(p, x, 4, 4 * fstride, batch, y, yv, p->ldy, 4 * yv, P.R + 1, false, S(stream)));
+  SW_TRY(ana_run(p, x, xl, batch, y, yv, p->ldy, 4 * yv, P.R + 1, false, S(stream)));
   return launch_finalize_divcurl(P, y, 4 * yv, p->ldy, reinterpret_cast<double2*>(div),
                                  reinterpret_cast<double2*>(curl), batch, S(stream));
 }
@@ -390,13 +406,15 @@ int swsdc_eval_fe(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, c
   if (batch == 0) return kOk;
   const bool nl = include_nonlinear != 0;
   const int nv = nl ? 7 : 2;
-  SW_TRY(ensure_ws(p, 5 * batch, nv * batch, nv * batch, S(stream)));
+  const size_t xb = x_bytes_for(p, nv, batch);
+  SW_TRY(ensure_ws(p, 5 * batch, xb, nv * batch, S(stream)));
   const PlanDev& P = p->dev;
   const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
   const long long plane = (long long)(P.R + 1) * (P.R + 1);
+  const XLayout xl = make_xlayout(P.R, P.Jh, nv);
   double2* eo = ws_eo(p);
-  double2* x = ws_x(p, 5 * batch);
-  double2* y = ws_y(p, 5 * batch, nv * batch);
+  double* x = ws_x(p, 5 * batch);
+  double2* y = ws_y(p, 5 * batch, xb);
   SynArgs a{};
   a.src = reinterpret_cast<const double2*>(state);
   a.src_fstride = plane;
@@ -408,11 +426,9 @@ int swsdc_eval_fe(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, c
   a.eo_mstride = 5 * fstride;
   a.nmembers = batch;
   SW_TRY(launch_synthesis(P, a, 5, kSynSWE, S(stream)));
-  SW_TRY(launch_swe_grid(P, nl, eo, 5 * fstride, x, nv * fstride, batch, q->omega, q->radius,
-                         S(stream)));
+  SW_TRY(launch_swe_grid(P, nl, eo, 5 * fstride, x, xl, batch, q->omega, q->radius, S(stream)));
   const long long yv = (long long)(P.R + 1) * p->ldy;
-  SW_TRY(ana_run(p, x, nv, nv * fstride, batch, y, yv, p->ldy, nv * yv, P.R + 1, false,
-                 S(stream)));
+  SW_TRY(ana_run(p, x, xl, batch, y, yv, p->ldy, nv * yv, P.R + 1, false, S(stream)));
   return launch_finalize_swe(P, y, nv * yv, p->ldy, reinterpret_cast<double2*>(out), 3 * plane, nl,
                              q->radius, batch, S(stream));
 }

@@ -75,8 +75,38 @@ struct PlanDev {
   const double2* ckpt;    // [sum_r nchunk(r)][Jh] (q_{s0}, q_{s0+1}) chunk seeds
   const int* ck_off;      // [R+1] first chunk index of row r in ckpt
   const double2* tw;      // [I] exp(-2 pi i e / I)
+  const int* rev;         // [I] padded ring slot of frequency k (digit-reversed DIF order)
+  int ring_stride;        // double2 slots per ring in shared memory (== 1 mod 8)
   swfft::FftPlan fft;
 };
+
+// Layout of the analysis input x (written by fourier.cu, read by the DMMA
+// analysis): vectors in groups of 16; per group, for each (r, block of 4
+// latitudes jb, parity p in {S, D}), nc = 8*NT real columns (re/im of each
+// vector) x 4 latitudes -- exactly one m8n8k4 B fragment per (jb, p, n-tile),
+// so a warp loads it with one coalesced 256-byte access.
+struct XLayout {
+  int nv;          // vectors
+  int nc;          // columns per group (8 * n-tiles of a full group)
+  int jh4;         // ceil(Jh / 4)
+  long long gstride;  // doubles per group of 16 vectors
+  long long mstride;  // doubles per member
+  __host__ __device__ size_t idx(int v, int comp, int r, int jh, int p) const {
+    const int g = v >> 4, n = 2 * (v & 15) + comp;
+    return (size_t)g * gstride + ((((size_t)r * jh4 + (jh >> 2)) * 2 + p) * nc + n) * 4 + (jh & 3);
+  }
+};
+
+inline XLayout make_xlayout(int R, int Jh, int nv) {
+  XLayout L;
+  L.nv = nv;
+  const int nfull = nv < 16 ? nv : 16;
+  L.nc = 8 * ((2 * nfull + 7) / 8);
+  L.jh4 = (Jh + 3) / 4;
+  L.gstride = (long long)(R + 1) * L.jh4 * 2 * L.nc * 4;
+  L.mstride = L.gstride * ((nv + 15) / 16);
+  return L;
+}
 
 __host__ __device__ inline int jn_of(const PlanDev& p, int jh) { return p.J - p.Jh + jh; }
 __host__ __device__ inline int js_of(const PlanDev& p, int jh) { return p.J - 1 - jn_of(p, jh); }

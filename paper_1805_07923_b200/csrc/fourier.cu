@@ -19,23 +19,28 @@
 // Fourier-space weights (w, w/(1-mu^2), i r, 1/a) of the div/curl/analysis
 // contractions (spharm.py:201-205, 281-300) are applied before the result is
 // written for the Legendre analysis.
+//
+// Rings are padded (fft_core.cuh) with a ring stride == 1 (mod 8) double2, so
+// both the butterflies and the cross-ring grid transposes are bank-conflict
+// free.  Pairs per CTA (np) is a power of two.
+#include <algorithm>
+
 #include "common.cuh"
 #include "fourier.cuh"
 
 namespace swsdc {
 namespace {
 
-template <bool BIGP>
-__device__ __forceinline__ void fft_stage_all(double2* rings, int nrings, const PlanDev& P, int s,
-                                              bool inverse) {
+template <bool BIGP, bool INV>
+__device__ __forceinline__ void fft_stage_all(double2* rings, int nrings, const PlanDev& P, int s) {
   const swfft::FftPlan& fp = P.fft;
   const int r = fp.radix[s];
   const int nb = fp.n / r;
   const int total = nrings * nb;
   for (int t = threadIdx.x; t < total; t += blockDim.x) {
-    const int q = t / nb, b = t - q * nb;
-    double2* ring = rings + (size_t)q * fp.n;
-    swfft::stage_butterfly<BIGP>(ring, fp, s, b, P.tw, inverse);
+    const int q = (nb == 1) ? t : (int)swfft::udiv((uint32_t)t, fp.bmag[s]);
+    const int b = t - q * nb;
+    swfft::stage_butterfly<BIGP, INV>(rings + (size_t)q * P.ring_stride, fp, s, b, P.tw);
   }
 }
 
@@ -43,7 +48,7 @@ __device__ __forceinline__ void fft_stage_all(double2* rings, int nrings, const 
 template <bool BIGP>
 __device__ void fft_forward(double2* rings, int nrings, const PlanDev& P) {
   for (int s = 0; s < P.fft.nstage; ++s) {
-    fft_stage_all<BIGP>(rings, nrings, P, s, false);
+    fft_stage_all<BIGP, false>(rings, nrings, P, s);
     __syncthreads();
   }
 }
@@ -51,24 +56,59 @@ __device__ void fft_forward(double2* rings, int nrings, const PlanDev& P) {
 template <bool BIGP>
 __device__ void fft_inverse(double2* rings, int nrings, const PlanDev& P) {
   for (int s = P.fft.nstage - 1; s >= 0; --s) {
-    fft_stage_all<BIGP>(rings, nrings, P, s, true);
+    fft_stage_all<BIGP, true>(rings, nrings, P, s);
     __syncthreads();
   }
 }
 
-__device__ __forceinline__ void zero_rings(double2* rings, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) rings[i] = make_double2(0.0, 0.0);
+__device__ __forceinline__ double2 d2(double x, double y) { return make_double2(x, y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return d2(a.x * s, a.y * s); }
+// i r s * a
+__device__ __forceinline__ double2 ir_scale(double2 a, double rs) { return d2(-a.y * rs, a.x * rs); }
+__device__ __forceinline__ double2 cadd2(double2 a, double2 b) { return d2(a.x + b.x, a.y + b.y); }
+
+// Packed ring values at +r and -r from a pair's (E, O) partial sums.
+__device__ __forceinline__ void pair_spectrum(double2 E, double2 O, int r, double2& zp,
+                                              double2& zm) {
+  const double2 Fn = d2(E.x + O.x, E.y + O.y), Fs = d2(E.x - O.x, E.y - O.y);
+  if (r == 0) {
+    zp = d2(Fn.x, Fs.x);  // irfft drops Im of the DC bin
+    zm = zp;
+  } else {
+    zp = d2(Fn.x - Fs.y, Fn.y + Fs.x);   // F_n + i F_s
+    zm = d2(Fn.x + Fs.y, Fs.x - Fn.y);   // conj(F_n) + i conj(F_s)
+  }
 }
 
-// Place the spectra of a pair (F_n, F_s at wavenumber r) into a packed ring
-// in digit-reversed order.
-__device__ __forceinline__ void put_pair(double2* ring, const PlanDev& P, int r, double2 Fn,
-                                         double2 Fs) {
-  if (r == 0) {
-    ring[0] = make_double2(Fn.x, Fs.x);  // irfft drops Im of the DC bin
-  } else {
-    ring[swfft::digit_rev(P.fft, r)] = make_double2(Fn.x - Fs.y, Fn.y + Fs.x);
-    ring[swfft::digit_rev(P.fft, P.I - r)] = make_double2(Fn.x + Fs.y, Fs.x - Fn.y);
+// Fill nr rings (ring q of CTA-local pair i at rings[(q*np + i) * RS]) from
+// (E, O) rows eo[q][r][jh0 + i]; every slot is written (zeros off-band).
+__device__ __forceinline__ void fill_rings(double2* rings, const PlanDev& P, const double2* eo,
+                                           size_t fstride, int nr, int np, int lnp, int jh0) {
+  const int R = P.R, I = P.I, RS = P.ring_stride;
+  const int nband = (nr * (R + 1)) << lnp;
+  const int nmid = I - 2 * R - 1;
+  const int nzero = (nr * nmid) << lnp;
+  for (int idx = threadIdx.x; idx < nband + nzero; idx += blockDim.x) {
+    if (idx < nband) {
+      const int i = idx & (np - 1);
+      const int qr = idx >> lnp;
+      const int q = qr / (R + 1), r = qr - q * (R + 1);
+      const int jh = jh0 + i;
+      double2* ring = rings + (size_t)(q * np + i) * RS;
+      double2 zp = d2(0.0, 0.0), zm = zp;
+      if (jh < P.Jh) {
+        const double2* src = eo + q * fstride + ((size_t)r * P.Jh + jh) * 2;
+        pair_spectrum(src[0], src[1], r, zp, zm);
+      }
+      ring[P.rev[r]] = zp;
+      if (r != 0) ring[P.rev[I - r]] = zm;
+    } else {
+      const int z = idx - nband;
+      const int i = z & (np - 1);
+      const int qk = z >> lnp;
+      const int q = qk / nmid, k = R + 1 + (qk - q * nmid);
+      rings[(size_t)(q * np + i) * RS + P.rev[k]] = d2(0.0, 0.0);
+    }
   }
 }
 
@@ -76,58 +116,50 @@ __device__ __forceinline__ void put_pair(double2* ring, const PlanDev& P, int r,
 // transformed packed ring.
 __device__ __forceinline__ void get_pair(const double2* ring, const PlanDev& P, int r, double2& Fn,
                                          double2& Fs) {
-  const double2 zk = ring[swfft::digit_rev(P.fft, r)];
-  const double2 zm = ring[swfft::digit_rev(P.fft, r == 0 ? 0 : P.I - r)];
+  const double2 zk = ring[P.rev[r]];
+  const double2 zm = ring[P.rev[r == 0 ? 0 : P.I - r]];
   const double h = 0.5 / P.I;
-  Fn = make_double2((zk.x + zm.x) * h, (zk.y - zm.y) * h);
-  Fs = make_double2((zk.y + zm.y) * h, (zm.x - zk.x) * h);
+  Fn = d2((zk.x + zm.x) * h, (zk.y - zm.y) * h);
+  Fs = d2((zk.y + zm.y) * h, (zm.x - zk.x) * h);
 }
 
-__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
-// i r s * a
-__device__ __forceinline__ double2 ir_scale(double2 a, double rs) { return make_double2(-a.y * rs, a.x * rs); }
-__device__ __forceinline__ double2 cadd2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-
-// Write one analysis vector (S, D) from its north / south values.
-__device__ __forceinline__ void put_sd(double2* x, double2 vn, double2 vs, bool equator) {
+// Write analysis vector v at (r, jh): S = v_n + v_s, D = v_n - v_s (equator:
+// S = v_n, D = 0) into the fragment-native layout (common.cuh XLayout).
+__device__ __forceinline__ void put_x(double* x, const XLayout& L, int v, int r, int jh,
+                                      double2 vn, double2 vs, bool equator) {
+  double2 S, D;
   if (equator) {
-    x[0] = vn;
-    x[1] = make_double2(0.0, 0.0);
+    S = vn;
+    D = d2(0.0, 0.0);
   } else {
-    x[0] = make_double2(vn.x + vs.x, vn.y + vs.y);
-    x[1] = make_double2(vn.x - vs.x, vn.y - vs.y);
+    S = d2(vn.x + vs.x, vn.y + vs.y);
+    D = d2(vn.x - vs.x, vn.y - vs.y);
   }
+  x[L.idx(v, 0, r, jh, 0)] = S.x;
+  x[L.idx(v, 1, r, jh, 0)] = S.y;
+  x[L.idx(v, 0, r, jh, 1)] = D.x;
+  x[L.idx(v, 1, r, jh, 1)] = D.y;
 }
 
 // ---------------------------------------------------------------------------
 // (E, O) -> grid, np pairs per CTA.  grid: [f][I][J]
 // ---------------------------------------------------------------------------
 template <bool BIGP>
-__global__ void f2g_kernel(PlanDev P, const double2* eo, long long eo_fstride, double* grid,
-                           long long grid_fstride, int np) {
+__global__ void __launch_bounds__(256, 2) f2g_kernel(PlanDev P, const double2* eo, long long eo_fstride, double* grid,
+                           long long grid_fstride, int lnp) {
   extern __shared__ __align__(16) double2 rings[];
+  const int np = 1 << lnp;
   const int f = blockIdx.y;
   const int jh0 = blockIdx.x * np;
-  const double2* e = eo + (size_t)f * eo_fstride;
-  double* g = grid + (size_t)f * grid_fstride;
-  zero_rings(rings, np * P.I);
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < np * (P.R + 1); idx += blockDim.x) {
-    const int r = idx / np, i = idx - r * np;
-    const int jh = jh0 + i;
-    if (jh >= P.Jh) continue;
-    const double2* src = e + ((size_t)r * P.Jh + jh) * 2;
-    const double2 E = src[0], O = src[1];
-    put_pair(rings + (size_t)i * P.I, P, r, make_double2(E.x + O.x, E.y + O.y),
-             make_double2(E.x - O.x, E.y - O.y));
-  }
+  fill_rings(rings, P, eo + (size_t)f * eo_fstride, 0, 1, np, lnp, jh0);
   __syncthreads();
   fft_inverse<BIGP>(rings, np, P);
-  for (int idx = threadIdx.x; idx < np * P.I; idx += blockDim.x) {
-    const int il = idx / np, i = idx - il * np;
+  double* g = grid + (size_t)f * grid_fstride;
+  for (int idx = threadIdx.x; idx < (P.I << lnp); idx += blockDim.x) {
+    const int il = idx >> lnp, i = idx & (np - 1);
     const int jh = jh0 + i;
     if (jh >= P.Jh) continue;
-    const double2 z = rings[(size_t)i * P.I + il];
+    const double2 z = rings[(size_t)i * P.ring_stride + swfft::pad_idx(il)];
     const int jn = jn_of(P, jh), js = js_of(P, jh);
     g[(size_t)il * P.J + jn] = z.x;
     if (js != jn) g[(size_t)il * P.J + js] = z.y;
@@ -140,52 +172,52 @@ __global__ void f2g_kernel(PlanDev P, const double2* eo, long long eo_fstride, d
 // [P-div, H-div, P-curl, H-curl], weight w / (1 - mu^2)).
 // ---------------------------------------------------------------------------
 template <int MODE, bool BIGP>
-__global__ void g2f_kernel(PlanDev P, const double* grid, const double* grid2,
-                           long long grid_fstride, double2* x, long long x_fstride, int np) {
+__global__ void __launch_bounds__(256, 2) g2f_kernel(PlanDev P, const double* grid, const double* grid2,
+                           long long grid_fstride, double* x, XLayout xl, int lnp) {
   constexpr int NIN = (MODE == 0) ? 1 : 2;
-  extern __shared__ __align__(16) double2 rings[];  // [NIN][np][I]
+  extern __shared__ __align__(16) double2 rings[];  // [NIN][np][RS]
+  const int np = 1 << lnp;
   const int f = blockIdx.y;
   const int jh0 = blockIdx.x * np;
   const double* gin[2] = {grid + (size_t)f * grid_fstride,
                           (MODE == 0 ? grid : grid2) + (size_t)f * grid_fstride};
-  for (int idx = threadIdx.x; idx < NIN * np * P.I; idx += blockDim.x) {
-    const int q = idx / (np * P.I);
-    const int rem = idx - q * np * P.I;
-    const int il = rem / np, i = rem - il * np;
+  for (int idx = threadIdx.x; idx < NIN * (P.I << lnp); idx += blockDim.x) {
+    const int q = (NIN == 1) ? 0 : idx / (P.I << lnp);
+    const int rem = idx - q * (P.I << lnp);
+    const int il = rem >> lnp, i = rem & (np - 1);
     const int jh = jh0 + i;
-    double2 z = make_double2(0.0, 0.0);
+    double2 z = d2(0.0, 0.0);
     if (jh < P.Jh) {
       const double* gq = gin[q] + (size_t)il * P.J;
-      z = make_double2(gq[jn_of(P, jh)], gq[js_of(P, jh)]);
+      z = d2(gq[jn_of(P, jh)], gq[js_of(P, jh)]);
     }
-    rings[((size_t)q * np + i) * P.I + il] = z;
+    rings[(size_t)(q * np + i) * P.ring_stride + swfft::pad_idx(il)] = z;
   }
   __syncthreads();
   fft_forward<BIGP>(rings, NIN * np, P);
-  double2* xf = x + (size_t)f * x_fstride;
-  const size_t vstride = (size_t)(P.R + 1) * P.Jh * 2;
-  for (int idx = threadIdx.x; idx < np * (P.R + 1); idx += blockDim.x) {
-    const int r = idx / np, i = idx - r * np;
+  // mode 0: field f is vector f of one member; mode 1: pair f is member f (4 vectors)
+  double* xf = x + (MODE == 0 ? 0 : (size_t)f * xl.mstride);
+  for (int idx = threadIdx.x; idx < ((P.R + 1) << lnp); idx += blockDim.x) {
+    const int r = idx >> lnp, i = idx & (np - 1);
     const int jh = jh0 + i;
     if (jh >= P.Jh) continue;
     const bool eq = (jn_of(P, jh) == js_of(P, jh));
     const double mu = P.mu_n[jh], w = P.w_n[jh];
-    double2* xo = xf + ((size_t)r * P.Jh + jh) * 2;
     if (MODE == 0) {
       double2 Fn, Fs;
-      get_pair(rings + (size_t)i * P.I, P, r, Fn, Fs);
-      put_sd(xo, cscale(Fn, w), cscale(Fs, w), eq);
+      get_pair(rings + (size_t)i * P.ring_stride, P, r, Fn, Fs);
+      put_x(xf, xl, f, r, jh, cscale(Fn, w), cscale(Fs, w), eq);
     } else {
       double2 Un, Us, Vn, Vs;
-      get_pair(rings + (size_t)i * P.I, P, r, Un, Us);
-      get_pair(rings + (size_t)(np + i) * P.I, P, r, Vn, Vs);
+      get_pair(rings + (size_t)i * P.ring_stride, P, r, Un, Us);
+      get_pair(rings + (size_t)(np + i) * P.ring_stride, P, r, Vn, Vs);
       const double wc = w / (1.0 - mu * mu);
       const double rw = r * wc;
       // div = Pwc2 (i r F_U) - Hwc2 F_V ; curl = Pwc2 (i r F_V) + Hwc2 F_U  (spharm.py:294-299)
-      put_sd(xo, ir_scale(Un, rw), ir_scale(Us, rw), eq);
-      put_sd(xo + vstride, cscale(Vn, -wc), cscale(Vs, -wc), eq);
-      put_sd(xo + 2 * vstride, ir_scale(Vn, rw), ir_scale(Vs, rw), eq);
-      put_sd(xo + 3 * vstride, cscale(Un, wc), cscale(Us, wc), eq);
+      put_x(xf, xl, 0, r, jh, ir_scale(Un, rw), ir_scale(Us, rw), eq);
+      put_x(xf, xl, 1, r, jh, cscale(Vn, -wc), cscale(Vs, -wc), eq);
+      put_x(xf, xl, 2, r, jh, ir_scale(Vn, rw), ir_scale(Vs, rw), eq);
+      put_x(xf, xl, 3, r, jh, cscale(Un, wc), cscale(Us, wc), eq);
     }
   }
 }
@@ -196,26 +228,16 @@ __global__ void g2f_kernel(PlanDev P, const double* grid, const double* grid2,
 //   out: x[m][NV][R+1][Jh][2], NV = 7 (nonlinear) or 2 (linear only)
 // ---------------------------------------------------------------------------
 template <bool NONLIN, bool BIGP>
-__global__ void swe_grid_kernel(PlanDev P, const double2* eo, long long eo_mstride, double2* x,
-                                long long x_mstride, double omega, double radius) {
+__global__ void __launch_bounds__(256, 2) swe_grid_kernel(PlanDev P, const double2* eo, long long eo_mstride, double* x,
+                                XLayout xl, double omega, double radius) {
   constexpr int NIN = NONLIN ? 5 : 4;
   constexpr int NPROD = NONLIN ? 7 : 2;
-  constexpr int NR = NONLIN ? 7 : 4;
-  extern __shared__ __align__(16) double2 rings[];  // [NR][I]
+  extern __shared__ __align__(16) double2 rings[];  // [7 or 4][RS]
   const int jh = blockIdx.x;
   const int m = blockIdx.y;
-  const int I = P.I;
-  const double2* e = eo + (size_t)m * eo_mstride;
+  const int RS = P.ring_stride;
   const size_t fstride = (size_t)(P.R + 1) * P.Jh * 2;
-  zero_rings(rings, NIN * I);
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < NIN * (P.R + 1); idx += blockDim.x) {
-    const int q = idx / (P.R + 1), r = idx - q * (P.R + 1);
-    const double2* src = e + q * fstride + ((size_t)r * P.Jh + jh) * 2;
-    const double2 E = src[0], O = src[1];
-    put_pair(rings + (size_t)q * I, P, r, make_double2(E.x + O.x, E.y + O.y),
-             make_double2(E.x - O.x, E.y - O.y));
-  }
+  fill_rings(rings, P, eo + (size_t)m * eo_mstride + (size_t)jh * 2, fstride, NIN, 1, 0, 0);
   __syncthreads();
   fft_inverse<BIGP>(rings, NIN, P);
 
@@ -223,20 +245,20 @@ __global__ void swe_grid_kernel(PlanDev P, const double2* eo, long long eo_mstri
   const double fn = 2.0 * omega * mu;         // f = 2 Omega mu (swe.py:178); south: -fn
   const double c2o = 2.0 * omega / radius;    // swe.py:179
   const double ic2 = 1.0 / (1.0 - mu * mu);   // swe.py:180
-  for (int il = threadIdx.x; il < I; il += blockDim.x) {
-    const double2 U = rings[il], V = rings[I + il], Z = rings[2 * I + il], D = rings[3 * I + il];
+  for (int il = threadIdx.x; il < P.I; il += blockDim.x) {
+    const int p = swfft::pad_idx(il);
+    const double2 U = rings[p], V = rings[RS + p], Z = rings[2 * RS + p], D = rings[3 * RS + p];
     // swe.py:262,265 : tend_zeta grid = -f delta - (2 Omega/a) V ; tend_delta grid = f zeta - (2 Omega/a) U
-    rings[il] = make_double2(-fn * D.x - c2o * V.x, fn * D.y - c2o * V.y);
-    rings[I + il] = make_double2(fn * Z.x - c2o * U.x, -fn * Z.y - c2o * U.y);
+    rings[p] = d2(-fn * D.x - c2o * V.x, fn * D.y - c2o * V.y);
+    rings[RS + p] = d2(fn * Z.x - c2o * U.x, -fn * Z.y - c2o * U.y);
     if (NONLIN) {
-      const double2 Ph = rings[4 * I + il];
+      const double2 Ph = rings[4 * RS + p];
       // swe.py:271-273 : Phi U, Phi V, zeta U, zeta V, KE = (U^2 + V^2) / (2 (1 - mu^2))
-      rings[2 * I + il] = make_double2(Ph.x * U.x, Ph.y * U.y);
-      rings[3 * I + il] = make_double2(Ph.x * V.x, Ph.y * V.y);
-      rings[4 * I + il] = make_double2(Z.x * U.x, Z.y * U.y);
-      rings[5 * I + il] = make_double2(Z.x * V.x, Z.y * V.y);
-      rings[6 * I + il] = make_double2(0.5 * (U.x * U.x + V.x * V.x) * ic2,
-                                       0.5 * (U.y * U.y + V.y * V.y) * ic2);
+      rings[2 * RS + p] = d2(Ph.x * U.x, Ph.y * U.y);
+      rings[3 * RS + p] = d2(Ph.x * V.x, Ph.y * V.y);
+      rings[4 * RS + p] = d2(Z.x * U.x, Z.y * U.y);
+      rings[5 * RS + p] = d2(Z.x * V.x, Z.y * V.y);
+      rings[6 * RS + p] = d2(0.5 * (U.x * U.x + V.x * V.x) * ic2, 0.5 * (U.y * U.y + V.y * V.y) * ic2);
     }
   }
   __syncthreads();
@@ -246,42 +268,47 @@ __global__ void swe_grid_kernel(PlanDev P, const double2* eo, long long eo_mstri
   const double w = P.w_n[jh];
   const double wc = w * ic2;
   const double ia = 1.0 / radius;
-  double2* xm = x + (size_t)m * x_mstride;
+  double* xm = x + (size_t)m * xl.mstride;
   for (int r = threadIdx.x; r <= P.R; r += blockDim.x) {
     double2 A1n, A1s, A2n, A2s;
     get_pair(rings, P, r, A1n, A1s);
-    get_pair(rings + I, P, r, A2n, A2s);
-    double2* xo = xm + ((size_t)r * P.Jh + jh) * 2;
+    get_pair(rings + RS, P, r, A2n, A2s);
     if (!NONLIN) {
-      put_sd(xo, cscale(A1n, w), cscale(A1s, w), eq);
-      put_sd(xo + fstride, cscale(A2n, w), cscale(A2s, w), eq);
+      put_x(xm, xl, 0, r, jh, cscale(A1n, w), cscale(A1s, w), eq);
+      put_x(xm, xl, 1, r, jh, cscale(A2n, w), cscale(A2s, w), eq);
     } else {
       double2 PUn, PUs, PVn, PVs, ZUn, ZUs, ZVn, ZVs, Kn, Ks;
-      get_pair(rings + 2 * I, P, r, PUn, PUs);
-      get_pair(rings + 3 * I, P, r, PVn, PVs);
-      get_pair(rings + 4 * I, P, r, ZUn, ZUs);
-      get_pair(rings + 5 * I, P, r, ZVn, ZVs);
-      get_pair(rings + 6 * I, P, r, Kn, Ks);
+      get_pair(rings + 2 * RS, P, r, PUn, PUs);
+      get_pair(rings + 3 * RS, P, r, PVn, PVs);
+      get_pair(rings + 4 * RS, P, r, ZUn, ZUs);
+      get_pair(rings + 5 * RS, P, r, ZVn, ZVs);
+      get_pair(rings + 6 * RS, P, r, Kn, Ks);
       const double rwa = r * wc * ia, wa = wc * ia;
       // P-vectors: phi, zeta, delta, ke ; H-vectors: phi, zeta, delta
-      put_sd(xo, ir_scale(PUn, -rwa), ir_scale(PUs, -rwa), eq);
-      put_sd(xo + fstride, cadd2(cscale(A1n, w), ir_scale(ZUn, -rwa)),
-             cadd2(cscale(A1s, w), ir_scale(ZUs, -rwa)), eq);
-      put_sd(xo + 2 * fstride, cadd2(cscale(A2n, w), ir_scale(ZVn, rwa)),
-             cadd2(cscale(A2s, w), ir_scale(ZVs, rwa)), eq);
-      put_sd(xo + 3 * fstride, cscale(Kn, w), cscale(Ks, w), eq);
-      put_sd(xo + 4 * fstride, cscale(PVn, wa), cscale(PVs, wa), eq);
-      put_sd(xo + 5 * fstride, cscale(ZVn, wa), cscale(ZVs, wa), eq);
-      put_sd(xo + 6 * fstride, cscale(ZUn, wa), cscale(ZUs, wa), eq);
+      put_x(xm, xl, 0, r, jh, ir_scale(PUn, -rwa), ir_scale(PUs, -rwa), eq);
+      put_x(xm, xl, 1, r, jh, cadd2(cscale(A1n, w), ir_scale(ZUn, -rwa)),
+            cadd2(cscale(A1s, w), ir_scale(ZUs, -rwa)), eq);
+      put_x(xm, xl, 2, r, jh, cadd2(cscale(A2n, w), ir_scale(ZVn, rwa)),
+            cadd2(cscale(A2s, w), ir_scale(ZVs, rwa)), eq);
+      put_x(xm, xl, 3, r, jh, cscale(Kn, w), cscale(Ks, w), eq);
+      put_x(xm, xl, 4, r, jh, cscale(PVn, wa), cscale(PVs, wa), eq);
+      put_x(xm, xl, 5, r, jh, cscale(ZVn, wa), cscale(ZVs, wa), eq);
+      put_x(xm, xl, 6, r, jh, cscale(ZUn, wa), cscale(ZUs, wa), eq);
     }
   }
 }
 
 int pick_threads(int work, bool bigp) {
   if (bigp) return work >= 128 ? 128 : 64;
-  if (work >= 512) return 256;
+  if (work >= 256) return 256;
   if (work >= 128) return 128;
   return 64;
+}
+
+int max_butterflies(const PlanDev& P) {
+  int mx = 1;
+  for (int s = 0; s < P.fft.nstage; ++s) mx = std::max(mx, P.fft.n / P.fft.radix[s]);
+  return mx;
 }
 
 int set_smem(const void* kern, size_t smem) {
@@ -294,54 +321,53 @@ int set_smem(const void* kern, size_t smem) {
   return kOk;
 }
 
-int pairs_per_cta(const PlanDev& P, int nin) {
-  // keep the rings at <= ~96 KB so two CTAs fit per SM; at least one pair
-  int np = (int)((96 * 1024) / ((size_t)nin * P.I * sizeof(double2)));
-  if (np < 1) np = 1;
-  if (np > 8) np = 8;
-  if (np > P.Jh) np = P.Jh;
-  return np;
+// log2 of pairs per CTA: rings <= ~56 KB (4 CTAs/SM), at most 8 pairs
+int pairs_log2(const PlanDev& P, int nin) {
+  const size_t ring = sizeof(double2) * P.ring_stride * nin;
+  int l = 0;
+  while (l < 3 && ring * (2 << l) <= 56 * 1024 && (2 << l) <= P.Jh) ++l;
+  return l;
 }
 
 template <bool BIGP>
 int f2g_launch(const PlanDev& P, const double2* eo, long long eo_fstride, double* grid,
                long long grid_fstride, int nf, cudaStream_t st) {
-  const int np = pairs_per_cta(P, 1);
-  const size_t smem = sizeof(double2) * np * P.I;
+  const int lnp = pairs_log2(P, 1), np = 1 << lnp;
+  const size_t smem = sizeof(double2) * np * P.ring_stride;
   SW_TRY(set_smem((const void*)f2g_kernel<BIGP>, smem));
   dim3 gridDim((P.Jh + np - 1) / np, nf);
   StageScope sc("fourier_to_grid", st);
-  f2g_kernel<BIGP><<<gridDim, pick_threads(np * P.I / 4, BIGP), smem, st>>>(P, eo, eo_fstride, grid,
-                                                                       grid_fstride, np);
+  f2g_kernel<BIGP><<<gridDim, pick_threads(np * max_butterflies(P), BIGP), smem, st>>>(
+      P, eo, eo_fstride, grid, grid_fstride, lnp);
   SW_LAUNCH_CHECK();
   return kOk;
 }
 
 template <int MODE, bool BIGP>
 int g2f_launch(const PlanDev& P, const double* grid, const double* grid2, long long grid_fstride,
-               double2* x, long long x_fstride, int nf, cudaStream_t st) {
+               double* x, const XLayout& xl, int nf, cudaStream_t st) {
   const int nin = MODE == 0 ? 1 : 2;
-  const int np = pairs_per_cta(P, nin);
-  const size_t smem = sizeof(double2) * nin * np * P.I;
+  const int lnp = pairs_log2(P, nin), np = 1 << lnp;
+  const size_t smem = sizeof(double2) * nin * np * P.ring_stride;
   dim3 gridDim((P.Jh + np - 1) / np, nf);
   SW_TRY(set_smem((const void*)g2f_kernel<MODE, BIGP>, smem));
   StageScope sc(MODE == 0 ? "grid_to_fourier" : "grid_to_fourier_divcurl", st);
-  g2f_kernel<MODE, BIGP><<<gridDim, pick_threads(nin * np * P.I / 4, BIGP), smem, st>>>(
-      P, grid, grid2, grid_fstride, x, x_fstride, np);
+  g2f_kernel<MODE, BIGP><<<gridDim, pick_threads(nin * np * max_butterflies(P), BIGP), smem, st>>>(
+      P, grid, grid2, grid_fstride, x, xl, lnp);
   SW_LAUNCH_CHECK();
   return kOk;
 }
 
 template <bool NONLIN, bool BIGP>
-int swe_launch(const PlanDev& P, const double2* eo, long long eo_mstride, double2* x,
-               long long x_mstride, int nmembers, double omega, double radius, cudaStream_t st) {
+int swe_launch(const PlanDev& P, const double2* eo, long long eo_mstride, double* x,
+               const XLayout& xl, int nmembers, double omega, double radius, cudaStream_t st) {
   const int nr = NONLIN ? 7 : 4;
-  const size_t smem = sizeof(double2) * nr * P.I;
+  const size_t smem = sizeof(double2) * nr * P.ring_stride;
   dim3 gridDim(P.Jh, nmembers);
   SW_TRY(set_smem((const void*)swe_grid_kernel<NONLIN, BIGP>, smem));
   StageScope sc("swe_grid", st);
-  swe_grid_kernel<NONLIN, BIGP><<<gridDim, pick_threads(nr * P.I / 4, BIGP), smem, st>>>(
-      P, eo, eo_mstride, x, x_mstride, omega, radius);
+  swe_grid_kernel<NONLIN, BIGP><<<gridDim, pick_threads(nr * max_butterflies(P), BIGP), smem, st>>>(
+      P, eo, eo_mstride, x, xl, omega, radius);
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -355,27 +381,27 @@ int launch_fourier_to_grid(const PlanDev& P, const double2* eo, long long eo_fst
 }
 
 int launch_grid_to_fourier(const PlanDev& P, int mode, const double* grid, const double* grid2,
-                           long long grid_fstride, double2* x, long long x_fstride, int nf,
+                           long long grid_fstride, double* x, const XLayout& xl, int nf,
                            cudaStream_t st) {
   const bool big = swfft::fft_needs_bigp(P.I);
   if (mode == 0) {
-    if (big) return g2f_launch<0, true>(P, grid, grid2, grid_fstride, x, x_fstride, nf, st);
-    return g2f_launch<0, false>(P, grid, grid2, grid_fstride, x, x_fstride, nf, st);
+    if (big) return g2f_launch<0, true>(P, grid, grid2, grid_fstride, x, xl, nf, st);
+    return g2f_launch<0, false>(P, grid, grid2, grid_fstride, x, xl, nf, st);
   }
-  if (big) return g2f_launch<1, true>(P, grid, grid2, grid_fstride, x, x_fstride, nf, st);
-  return g2f_launch<1, false>(P, grid, grid2, grid_fstride, x, x_fstride, nf, st);
+  if (big) return g2f_launch<1, true>(P, grid, grid2, grid_fstride, x, xl, nf, st);
+  return g2f_launch<1, false>(P, grid, grid2, grid_fstride, x, xl, nf, st);
 }
 
 int launch_swe_grid(const PlanDev& P, bool nonlinear, const double2* eo, long long eo_mstride,
-                    double2* x, long long x_mstride, int nmembers, double omega, double radius,
+                    double* x, const XLayout& xl, int nmembers, double omega, double radius,
                     cudaStream_t st) {
   const bool big = swfft::fft_needs_bigp(P.I);
   if (nonlinear) {
-    if (big) return swe_launch<true, true>(P, eo, eo_mstride, x, x_mstride, nmembers, omega, radius, st);
-    return swe_launch<true, false>(P, eo, eo_mstride, x, x_mstride, nmembers, omega, radius, st);
+    if (big) return swe_launch<true, true>(P, eo, eo_mstride, x, xl, nmembers, omega, radius, st);
+    return swe_launch<true, false>(P, eo, eo_mstride, x, xl, nmembers, omega, radius, st);
   }
-  if (big) return swe_launch<false, true>(P, eo, eo_mstride, x, x_mstride, nmembers, omega, radius, st);
-  return swe_launch<false, false>(P, eo, eo_mstride, x, x_mstride, nmembers, omega, radius, st);
+  if (big) return swe_launch<false, true>(P, eo, eo_mstride, x, xl, nmembers, omega, radius, st);
+  return swe_launch<false, false>(P, eo, eo_mstride, x, xl, nmembers, omega, radius, st);
 }
 
 }  // namespace swsdc

@@ -20,7 +20,8 @@
 //    applied in spectral.cu), both from spharm.py:171-178.
 //
 // Synthesis: DFMA register kernel, each lane owns 2 latitudes and runs the
-// recurrence in registers; coefficients are warp-uniform smem broadcasts.
+// recurrence in registers; coefficients are warp-uniform smem broadcasts from a
+// warp-private slab refilled chunk by chunk.
 // Analysis: the q tile (32 degrees x 128 latitudes) is generated into shared
 // memory and contracted over latitude with FP64 tensor-core DMMA
 // (mma.sync.m8n8k4.f64), so the latitude reduction happens inside the MMA.
@@ -75,12 +76,20 @@ int build_checkpoints(const PlanDev& P, const double* a_tab, const double* b_tab
 
 // ---------------------------------------------------------------------------
 // Synthesis
+//
+// One CTA per (r-pair {p, R-p}, latitude group of 64, member): the pair folds
+// the triangular work so every CTA carries R+4 recurrence steps.  NSPLIT warps
+// share the pair's chunks (a warp never straddles the two rows); each warp is
+// autonomous: lane l stages degree k0+l of its chunk (coefficients already
+// scaled by g, for B fields) into a warp-private smem slab while the next
+// chunk's coefficients, betas and seeds are in flight in registers.  Lanes own
+// 2 latitudes each; E/O accumulators stay in registers until the row ends.
 // ---------------------------------------------------------------------------
 namespace {
 
-constexpr int kSynWarps = 4;
-constexpr int kSynNL = 2;  // latitudes per lane
-constexpr int kSynLat = 32 * kSynNL;
+constexpr int kSynNL = 2;            // latitudes per lane
+constexpr int kSynLat = 32 * kSynNL; // latitudes per latitude group
+constexpr int kCS = kChunk + 2;      // staged degrees per chunk (+2 for the pair loop)
 
 __device__ __forceinline__ double2 fetch_coef(const double2* f, int srcR, int r, int s) {
   if (s < r || s > srcR || r > srcR) return make_double2(0.0, 0.0);
@@ -98,93 +107,139 @@ __device__ __forceinline__ double2 h_fold(const double2* f, int srcR, int r, int
 }
 
 __device__ __forceinline__ double inv_lap(int s, double radius) {
-  if (s == 0) return 0.0;
+  if (s <= 0) return 0.0;
   const double lam = (-(double)s * (s + 1.0)) / (radius * radius);
   return 1.0 / lam;
 }
 
-template <int B, int MODE>
-__device__ __forceinline__ void stage_coefs(const PlanDev& P, const SynArgs& a, int r, int nstep,
-                                            int npad, double2* cs) {
+// Coefficient of synthesis field b at (r, s) for the kernel mode (unscaled).
+template <int MODE>
+__device__ __forceinline__ double2 syn_coef(const PlanDev& P, const SynArgs& a, int b, int r, int s) {
   const double* eps_r = P.eps + (size_t)r * P.ldk;
+  if (MODE == kSynPlain) return fetch_coef(a.src + (size_t)b * a.src_fstride, a.src_R, r, s);
+  if (MODE == kSynUV) {
+    // U = i r chi - d(psi),  V = i r psi + d(chi)   (spharm.py:272-278)
+    const double2* psi = a.src;
+    const double2* chi = a.src2;
+    const double2 c = fetch_coef(b == 0 ? chi : psi, a.src_R, r, s);
+    const double2 h = h_fold(b == 0 ? psi : chi, a.src_R, r, s, eps_r, 1.0, 1.0);
+    const double sg = (b == 0) ? -1.0 : 1.0;
+    return make_double2(-r * c.y + sg * h.x, r * c.x + sg * h.y);
+  }
+  // kSynSWE: state (phi, zeta, delta) -> U/a, V/a, zeta, delta, phi
+  const double2* phi = a.src;
+  const double2* zeta = a.src + a.src_fstride;
+  const double2* delta = a.src + 2 * a.src_fstride;
+  if (b < 2) {
+    // psi = invlap(zeta), chi = invlap(delta) (swe.py:186-187), then 1/a (swe.py:189)
+    const double ia = 1.0 / a.radius;
+    const double2 cm = fetch_coef(b == 0 ? delta : zeta, a.src_R, r, s);
+    const double sm = inv_lap(s, a.radius) * ia;
+    const double2 hh = h_fold(b == 0 ? zeta : delta, a.src_R, r, s, eps_r,
+                              inv_lap(s + 1, a.radius) * ia, inv_lap(s - 1, a.radius) * ia);
+    const double sg = (b == 0) ? -1.0 : 1.0;
+    return make_double2(-r * cm.y * sm + sg * hh.x, r * cm.x * sm + sg * hh.y);
+  }
+  return fetch_coef(b == 2 ? zeta : (b == 3 ? delta : phi), a.src_R, r, s);
+}
+
+// Per-lane registers of one chunk in flight.
+template <int B>
+struct ChunkRegs {
+  double2 coef[B];   // degree k0 + lane
+  double2 coef_x;    // degree k0 + 32 + lane (lanes 0, 1)
+  double beta, beta_x;
+  double2 seed[kSynNL];
+};
+
+template <int B, int MODE>
+__device__ __forceinline__ void load_chunk(ChunkRegs<B>& c, const PlanDev& P, const SynArgs& a,
+                                           int r, int ci, int nstep, int lane, const int* jh) {
+  const int k0 = ci * kChunk;
   const double* g_r = P.gsc + (size_t)r * P.ldk;
-  for (int idx = threadIdx.x; idx < B * npad; idx += blockDim.x) {
-    const int b = idx / npad, k = idx - b * npad;
+  const double* b_r = P.beta + (size_t)r * P.ldk;
+  const int k = k0 + lane;
+  const double g = g_r[k];
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
     double2 v = make_double2(0.0, 0.0);
     if (k < nstep) {
-      const int s = r + k;
-      if (MODE == kSynPlain) {
-        v = fetch_coef(a.src + (size_t)b * a.src_fstride, a.src_R, r, s);
-      } else if (MODE == kSynUV) {
-        // U = i r chi - d(psi),  V = i r psi + d(chi)   (spharm.py:272-278)
-        const double2* psi = a.src;
-        const double2* chi = a.src2;
-        if (b == 0) {
-          const double2 c = fetch_coef(chi, a.src_R, r, s);
-          const double2 h = h_fold(psi, a.src_R, r, s, eps_r, 1.0, 1.0);
-          v = make_double2(-r * c.y - h.x, r * c.x - h.y);
-        } else {
-          const double2 c = fetch_coef(psi, a.src_R, r, s);
-          const double2 h = h_fold(chi, a.src_R, r, s, eps_r, 1.0, 1.0);
-          v = make_double2(-r * c.y + h.x, r * c.x + h.y);
-        }
-      } else {  // kSynSWE: state (phi, zeta, delta) -> U/a, V/a, zeta, delta, phi
-        const double2* phi = a.src;
-        const double2* zeta = a.src + a.src_fstride;
-        const double2* delta = a.src + 2 * a.src_fstride;
-        const double ia = 1.0 / a.radius;
-        if (b < 2) {
-          // psi = invlap(zeta), chi = invlap(delta)  (swe.py:186-187), then 1/a (swe.py:189)
-          const double2* fpsi = zeta;
-          const double2* fchi = delta;
-          const double2 cmain = fetch_coef(b == 0 ? fchi : fpsi, a.src_R, r, s);
-          const double smain = inv_lap(s, a.radius) * ia;
-          const double2 hh = h_fold(b == 0 ? fpsi : fchi, a.src_R, r, s, eps_r,
-                                    inv_lap(s + 1, a.radius) * ia, inv_lap(s - 1 < 0 ? 0 : s - 1, a.radius) * ia);
-          const double sg = (b == 0) ? -1.0 : 1.0;
-          v = make_double2(-r * cmain.y * smain + sg * hh.x, r * cmain.x * smain + sg * hh.y);
-        } else if (b == 2) {
-          v = fetch_coef(zeta, a.src_R, r, s);
-        } else if (b == 3) {
-          v = fetch_coef(delta, a.src_R, r, s);
-        } else {
-          v = fetch_coef(phi, a.src_R, r, s);
-        }
-      }
-      const double g = g_r[k];
+      v = syn_coef<MODE>(P, a, b, r, r + k);
       v.x *= g;
       v.y *= g;
     }
-    cs[idx] = v;
+    c.coef[b] = v;
   }
+  c.beta = b_r[k];
+  c.beta_x = (lane < 2) ? b_r[k + kChunk] : 0.0;
+  const int off = P.ck_off[r] + ci;
+#pragma unroll
+  for (int l = 0; l < kSynNL; ++l)
+    c.seed[l] = (jh[l] < P.Jh) ? P.ckpt[(size_t)off * P.Jh + jh[l]] : make_double2(0.0, 0.0);
 }
 
-template <int B, int MODE>
-__global__ void __launch_bounds__(kSynWarps * 32)
+template <int B>
+__device__ __forceinline__ void flush_row(double2 (&E)[B][kSynNL], double2 (&O)[B][kSynNL],
+                                          double2* dst, int lane) {
+  // dst: [B][kSynLat][2] (E, O) slab
+#pragma unroll
+  for (int b = 0; b < B; ++b)
+#pragma unroll
+    for (int l = 0; l < kSynNL; ++l) {
+      double2* d = dst + ((size_t)b * kSynLat + lane + 32 * l) * 2;
+      d[0] = E[b][l];
+      d[1] = O[b][l];
+      E[b][l] = make_double2(0.0, 0.0);
+      O[b][l] = make_double2(0.0, 0.0);
+    }
+}
+
+template <int B, int MODE, int NSPLIT>
+__global__ void __launch_bounds__(NSPLIT * 32)
 syn_kernel(PlanDev P, SynArgs a) {
   extern __shared__ __align__(16) double smem[];
-  a.src += (size_t)blockIdx.y * a.src_mstride;
-  if (a.src2) a.src2 += (size_t)blockIdx.y * a.src_mstride;
-  a.eo += (size_t)blockIdx.y * a.eo_mstride;
-  const int r = blockIdx.x / a.nJB;
-  const int jb = blockIdx.x - r * a.nJB;
-  const int nstep = a.smax - r + 1;
-  const int npad = ((nstep + 1) & ~1) + 2;
-  double2* cs = reinterpret_cast<double2*>(smem);              // [B][npad]
-  double* bs = reinterpret_cast<double*>(cs + B * npad);       // [npad + kChunk + 4]
-  double2* red = reinterpret_cast<double2*>(bs + npad + kChunk + 4);  // [B][kSynLat][2]
-
-  stage_coefs<B, MODE>(P, a, r, nstep, npad, cs);
-  const double* beta_r = P.beta + (size_t)r * P.ldk;
-  for (int k = threadIdx.x; k < npad + kChunk + 4; k += blockDim.x) bs[k] = beta_r[k];
-  __syncthreads();
-
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* cs = reinterpret_cast<double2*>(smem) + (size_t)warp * B * kCS;        // [B][kCS]
+  double* bs = reinterpret_cast<double*>(reinterpret_cast<double2*>(smem) + NSPLIT * B * kCS) +
+               (size_t)warp * kCS;                                               // [kCS]
+  double2* red = reinterpret_cast<double2*>(smem) + NSPLIT * B * kCS + (NSPLIT * kCS + 1) / 2;
+
+  a.src += (size_t)blockIdx.z * a.src_mstride;
+  if (a.src2) a.src2 += (size_t)blockIdx.z * a.src_mstride;
+  a.eo += (size_t)blockIdx.z * a.eo_mstride;
+
+  const int p = blockIdx.x, lg = blockIdx.y;
+  const int rows[2] = {p, P.R - p};
+  const bool two = rows[1] > rows[0];
+  int nst[2], nch[2];
+  for (int i = 0; i < 2; ++i) {
+    nst[i] = (i == 0 || two) ? a.smax - rows[i] + 1 : 0;
+    nch[i] = (nst[i] + kChunk - 1) / kChunk;
+  }
+  // warps -> (row, chunk range); a warp never straddles the rows
+  int wrow = 0, cb = 0, ce = 0;
+  if (NSPLIT == 1) {
+    wrow = -1;  // the single warp walks both rows
+  } else {
+    int w1 = two ? (NSPLIT * nch[0] + (nch[0] + nch[1]) / 2) / (nch[0] + nch[1]) : NSPLIT;
+    w1 = max(1, min(w1, two ? NSPLIT - 1 : NSPLIT));
+    if (warp < w1) {
+      wrow = 0;
+      cb = warp * nch[0] / w1;
+      ce = (warp + 1) * nch[0] / w1;
+    } else {
+      wrow = 1;
+      const int w2 = NSPLIT - w1, ww = warp - w1;
+      cb = ww * nch[1] / w2;
+      ce = (ww + 1) * nch[1] / w2;
+    }
+  }
+
   int jh[kSynNL];
   double mu[kSynNL];
 #pragma unroll
   for (int l = 0; l < kSynNL; ++l) {
-    jh[l] = jb * kSynLat + lane + 32 * l;
+    jh[l] = lg * kSynLat + lane + 32 * l;
     mu[l] = (jh[l] < P.Jh) ? P.mu_n[jh[l]] : 0.0;
   }
   double2 E[B][kSynNL], O[B][kSynNL];
@@ -193,114 +248,161 @@ syn_kernel(PlanDev P, SynArgs a) {
 #pragma unroll
     for (int l = 0; l < kSynNL; ++l) { E[b][l] = make_double2(0.0, 0.0); O[b][l] = E[b][l]; }
 
-  const int nchunk = (nstep + kChunk - 1) / kChunk;
-  const int off = P.ck_off[r];
-  for (int c = warp; c < nchunk; c += kSynWarps) {
-    const int k0 = c * kChunk;
-    const int kend = min(k0 + kChunk, nstep);
-    double qa[kSynNL], qb[kSynNL];
+  const int irow0 = (NSPLIT == 1) ? 0 : wrow;
+  const int irow1 = (NSPLIT == 1) ? (two ? 1 : 0) : wrow;
+  for (int ir = irow0; ir <= irow1; ++ir) {
+    const int r = rows[ir], nstep = nst[ir];
+    const int c0 = (NSPLIT == 1) ? 0 : cb, c1 = (NSPLIT == 1) ? nch[ir] : ce;
+    if (c0 < c1) {
+      ChunkRegs<B> nx;
+      load_chunk<B, MODE>(nx, P, a, r, c0, nstep, lane, jh);
+      for (int ci = c0; ci < c1; ++ci) {
+        __syncwarp();
 #pragma unroll
-    for (int l = 0; l < kSynNL; ++l) {
-      double2 sd = make_double2(0.0, 0.0);
-      if (jh[l] < P.Jh) sd = P.ckpt[(size_t)(off + c) * P.Jh + jh[l]];
-      qa[l] = sd.x;
-      qb[l] = sd.y;
-    }
+        for (int b = 0; b < B; ++b) {
+          cs[b * kCS + lane] = nx.coef[b];
+          if (lane < 2) cs[b * kCS + kChunk + lane] = make_double2(0.0, 0.0);
+        }
+        bs[lane] = nx.beta;
+        if (lane < 2) bs[kChunk + lane] = nx.beta_x;
+        double qa[kSynNL], qb[kSynNL];
+#pragma unroll
+        for (int l = 0; l < kSynNL; ++l) { qa[l] = nx.seed[l].x; qb[l] = nx.seed[l].y; }
+        __syncwarp();
+        if (ci + 1 < c1) load_chunk<B, MODE>(nx, P, a, r, ci + 1, nstep, lane, jh);
+        const int kn = min(kChunk, nstep - ci * kChunk);
 #pragma unroll 2
-    for (int k = k0; k < kend; k += 2) {
+        for (int kk = 0; kk < kn; kk += 2) {
 #pragma unroll
-      for (int b = 0; b < B; ++b) {
-        const double2 ce = cs[b * npad + k];
-        const double2 co = cs[b * npad + k + 1];
+          for (int b = 0; b < B; ++b) {
+            const double2 ce_ = cs[b * kCS + kk];
+            const double2 co_ = cs[b * kCS + kk + 1];
 #pragma unroll
-        for (int l = 0; l < kSynNL; ++l) {
-          E[b][l].x = fma(qa[l], ce.x, E[b][l].x);
-          E[b][l].y = fma(qa[l], ce.y, E[b][l].y);
-          O[b][l].x = fma(qb[l], co.x, O[b][l].x);
-          O[b][l].y = fma(qb[l], co.y, O[b][l].y);
+            for (int l = 0; l < kSynNL; ++l) {
+              E[b][l].x = fma(qa[l], ce_.x, E[b][l].x);
+              E[b][l].y = fma(qa[l], ce_.y, E[b][l].y);
+              O[b][l].x = fma(qb[l], co_.x, O[b][l].x);
+              O[b][l].y = fma(qb[l], co_.y, O[b][l].y);
+            }
+          }
+          const double2 bb = *reinterpret_cast<const double2*>(bs + kk + 2);
+#pragma unroll
+          for (int l = 0; l < kSynNL; ++l) {
+            qa[l] = fma(mu[l], qb[l], -bb.x * qa[l]);
+            qb[l] = fma(mu[l], qa[l], -bb.y * qb[l]);
+          }
         }
       }
-      const double2 bb = *reinterpret_cast<const double2*>(bs + k + 2);
-#pragma unroll
-      for (int l = 0; l < kSynNL; ++l) {
-        qa[l] = fma(mu[l], qb[l], -bb.x * qa[l]);
-        qb[l] = fma(mu[l], qa[l], -bb.y * qb[l]);
-      }
     }
-  }
-
-  // deterministic cross-warp reduction (fixed warp order)
-  for (int w = 0; w < kSynWarps; ++w) {
-    if (warp == w) {
+    if (NSPLIT == 1) {
+      // sole owner of the row: write (E, O) straight out
 #pragma unroll
       for (int b = 0; b < B; ++b)
 #pragma unroll
         for (int l = 0; l < kSynNL; ++l) {
-          double2* d = red + ((size_t)b * kSynLat + lane + 32 * l) * 2;
-          if (w == 0) {
-            d[0] = E[b][l];
-            d[1] = O[b][l];
-          } else {
-            d[0].x += E[b][l].x; d[0].y += E[b][l].y;
-            d[1].x += O[b][l].x; d[1].y += O[b][l].y;
+          if (jh[l] < P.Jh) {
+            double2* o = a.eo + (((size_t)b * (P.R + 1) + r) * P.Jh + jh[l]) * 2;
+            o[0] = E[b][l];
+            o[1] = O[b][l];
           }
+          E[b][l] = make_double2(0.0, 0.0);
+          O[b][l] = make_double2(0.0, 0.0);
         }
     }
-    __syncthreads();
   }
-  for (int idx = threadIdx.x; idx < B * kSynLat; idx += blockDim.x) {
-    const int b = idx / kSynLat, lj = idx - b * kSynLat;
-    const int j = jb * kSynLat + lj;
-    if (j < P.Jh) {
-      double2* o = a.eo + (((size_t)b * (P.R + 1) + r) * P.Jh + j) * 2;
-      o[0] = red[(size_t)idx * 2];
-      o[1] = red[(size_t)idx * 2 + 1];
+  if (NSPLIT > 1) {
+    // deterministic reduction of the warps' partial rows (fixed warp order)
+    flush_row<B>(E, O, red + (size_t)warp * B * kSynLat * 2, lane);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 2 * B * kSynLat; idx += blockDim.x) {
+      const int ir = idx / (B * kSynLat);
+      const int rem = idx - ir * B * kSynLat;
+      const int b = rem / kSynLat, lj = rem - b * kSynLat;
+      if (ir == 1 && !two) continue;
+      const int j = lg * kSynLat + lj;
+      if (j >= P.Jh) continue;
+      double2 e = make_double2(0.0, 0.0), o = e;
+      for (int w = 0; w < NSPLIT; ++w) {
+        // warp w's row
+        int w1 = two ? (NSPLIT * nch[0] + (nch[0] + nch[1]) / 2) / (nch[0] + nch[1]) : NSPLIT;
+        w1 = max(1, min(w1, two ? NSPLIT - 1 : NSPLIT));
+        if ((w < w1 ? 0 : 1) != ir) continue;
+        const double2* src = red + ((size_t)w * B * kSynLat + (size_t)b * kSynLat + lj) * 2;
+        e.x += src[0].x; e.y += src[0].y;
+        o.x += src[1].x; o.y += src[1].y;
+      }
+      double2* dst = a.eo + (((size_t)b * (P.R + 1) + rows[ir]) * P.Jh + j) * 2;
+      dst[0] = e;
+      dst[1] = o;
     }
   }
 }
 
-template <int B, int MODE>
-int launch_syn_t(const PlanDev& P, const SynArgs& a0, cudaStream_t st) {
-  SynArgs a = a0;
-  a.nJB = (P.Jh + kSynLat - 1) / kSynLat;
-  const int npad_max = ((a.smax + 2) & ~1) + 2;
-  const size_t smem = sizeof(double2) * B * npad_max + sizeof(double) * (npad_max + kChunk + 4) +
-                      sizeof(double2) * 2 * B * kSynLat;
-  auto kern = syn_kernel<B, MODE>;
-  if (smem > 48 * 1024) SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+template <int B, int MODE, int NSPLIT>
+int launch_syn_t(const PlanDev& P, const SynArgs& a, cudaStream_t st) {
+  const int npairs = P.R / 2 + 1;
+  const int nlg = (P.Jh + kSynLat - 1) / kSynLat;
+  size_t smem = sizeof(double2) * NSPLIT * B * kCS + sizeof(double) * (NSPLIT * kCS + 2);
+  if (NSPLIT > 1) smem += sizeof(double2) * NSPLIT * B * kSynLat * 2;
+  auto kern = syn_kernel<B, MODE, NSPLIT>;
+  if (smem > 48 * 1024)
+    SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   StageScope sc("legendre_synthesis", st);
-  kern<<<dim3((P.R + 1) * a.nJB, a.nmembers), kSynWarps * 32, smem, st>>>(P, a);
+  kern<<<dim3(npairs, nlg, a.nmembers), NSPLIT * 32, smem, st>>>(P, a);
   SW_LAUNCH_CHECK();
   return kOk;
+}
+
+// Warps per CTA so the grid offers ~2 resident warps per SM sub-partition.
+int pick_split(const PlanDev& P, int nmembers) {
+  const long long base = (long long)(P.R / 2 + 1) * ((P.Jh + kSynLat - 1) / kSynLat) * nmembers;
+  if (base >= 1000) return 1;
+  if (base >= 500) return 2;
+  return 4;
+}
+
+template <int B, int MODE>
+int launch_syn_b(const PlanDev& P, const SynArgs& a, cudaStream_t st) {
+  switch (pick_split(P, a.nmembers)) {
+    case 1: return launch_syn_t<B, MODE, 1>(P, a, st);
+    case 2: return launch_syn_t<B, MODE, 2>(P, a, st);
+    default: return launch_syn_t<B, MODE, 4>(P, a, st);
+  }
 }
 
 }  // namespace
 
 int launch_synthesis(const PlanDev& P, const SynArgs& a, int B, int mode, cudaStream_t st) {
-  if (mode == kSynUV) return launch_syn_t<2, kSynUV>(P, a, st);
-  if (mode == kSynSWE) return launch_syn_t<5, kSynSWE>(P, a, st);
+  if (mode == kSynUV) return launch_syn_b<2, kSynUV>(P, a, st);
+  if (mode == kSynSWE) return launch_syn_b<5, kSynSWE>(P, a, st);
   switch (B) {
-    case 1: return launch_syn_t<1, kSynPlain>(P, a, st);
-    case 2: return launch_syn_t<2, kSynPlain>(P, a, st);
-    case 3: return launch_syn_t<3, kSynPlain>(P, a, st);
-    case 4: return launch_syn_t<4, kSynPlain>(P, a, st);
-    case 5: return launch_syn_t<5, kSynPlain>(P, a, st);
-    case 6: return launch_syn_t<6, kSynPlain>(P, a, st);
-    case 7: return launch_syn_t<7, kSynPlain>(P, a, st);
-    case 8: return launch_syn_t<8, kSynPlain>(P, a, st);
+    case 1: return launch_syn_b<1, kSynPlain>(P, a, st);
+    case 2: return launch_syn_b<2, kSynPlain>(P, a, st);
+    case 3: return launch_syn_b<3, kSynPlain>(P, a, st);
+    case 4: return launch_syn_b<4, kSynPlain>(P, a, st);
+    case 5: return launch_syn_b<5, kSynPlain>(P, a, st);
+    case 6: return launch_syn_b<6, kSynPlain>(P, a, st);
   }
-  set_error("synthesis batch per launch must be 1..8");
+  set_error("synthesis batch per launch must be 1..6");
   return kUsage;
 }
-
 // ---------------------------------------------------------------------------
 // Analysis (DMMA)
+//
+// One warp per (r, 32-degree chunk, member); 4 warps per CTA take consecutive
+// chunks of the same r so their x loads hit the same L1 lines.  Each warp
+// walks the latitudes in blocks of 32: lane l regenerates q for the chunk's 32
+// degrees at latitude 32*jb32 + l (seeded from the checkpoint) into a
+// warp-private A tile (rows ordered parity-major), then 8 k-steps of
+// mma.sync.m8n8k4.f64 contract 4 latitudes each: A = q (even or odd degrees),
+// B = x fragment (one coalesced 256-byte load from the fragment-native layout
+// written by fourier.cu), C accumulates (S-parity rows with S, D with D).  No
+// CTA barriers; the latitude reduction happens inside the tensor core.
 // ---------------------------------------------------------------------------
 namespace {
 
-constexpr int kAnaThreads = 128;
-constexpr int kAnaJC = 128;               // latitudes per smem tile
-constexpr int kAnaQS = kAnaJC + 4;        // q-tile row stride (doubles), == 4 mod 16
+constexpr int kAnaWarps = 4;
+constexpr int kQS = kChunk + 4;   // A-tile row stride (doubles), == 4 mod 16
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -309,125 +411,129 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 }
 
 template <int NT>
-__global__ void __launch_bounds__(kAnaThreads)
+__global__ void __launch_bounds__(kAnaWarps * 32)
 ana_kernel(PlanDev P, AnaArgs a) {
-  constexpr int XS = 8 * NT + 4;  // x-tile row stride (doubles)
   extern __shared__ __align__(16) double smem[];
-  double* qs = smem;                          // [32][kAnaQS]   rows ordered (parity, k/2)
-  double* xs = qs + 32 * kAnaQS;              // [2][kAnaJC][XS]  parity 0: S, 1: D
-  double* bs = xs + 2 * kAnaJC * XS;          // [kChunk]
-
-  a.x += (size_t)blockIdx.y * a.x_mstride;
-  a.out += (size_t)blockIdx.y * a.out_mstride;
-  const int2 wk = a.work[blockIdx.x];
-  const int r = wk.x, c = wk.y;
-  const int k0 = c * kChunk;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int par = warp & 1, half = warp >> 1;
+  double* qs = smem + (size_t)warp * (kChunk * kQS + kChunk);   // [32][kQS]
+  double* bs = qs + kChunk * kQS;                                // [32] betas
 
-  for (int i = tid; i < kChunk; i += kAnaThreads) bs[i] = P.beta[(size_t)r * P.ldk + k0 + i];
-  // zero the padding columns once
-  for (int i = tid; i < 2 * kAnaJC * XS; i += kAnaThreads) xs[i] = 0.0;
+  const double* x = a.x + (size_t)blockIdx.y * a.xl.mstride;
+  double2* out = a.out + (size_t)blockIdx.y * a.out_mstride;
+  const int2 wk = a.work[blockIdx.x];
+  const int r = wk.x, c = wk.y + warp;
+  const int nout = a.smax - r + 1;
 
-  double acc[NT][2];
-#pragma unroll
-  for (int n = 0; n < NT; ++n) { acc[n][0] = 0.0; acc[n][1] = 0.0; }
-
-  const int off = P.ck_off[r];
-  const size_t xrow = (size_t)(P.R + 1) * P.Jh * 2;  // per-vector stride in double2
-  for (int jc0 = 0; jc0 < P.Jh; jc0 += kAnaJC) {
-    __syncthreads();
-    // stage x (S, D) for nv vectors
-    for (int idx = tid; idx < kAnaJC * a.nv; idx += kAnaThreads) {
-      const int v = idx / kAnaJC, jl = idx - v * kAnaJC;
-      const int j = jc0 + jl;
-      double2 S = make_double2(0.0, 0.0), D = S;
-      if (j < P.Jh) {
-        const double2* src = a.x + v * xrow + ((size_t)r * P.Jh + j) * 2;
-        S = src[0];
-        D = src[1];
-      }
-      double* x0 = xs + (size_t)jl * XS + 2 * v;
-      double* x1 = xs + (size_t)(kAnaJC + jl) * XS + 2 * v;
-      x0[0] = S.x; x0[1] = S.y;
-      x1[0] = D.x; x1[1] = D.y;
+  if (a.zero_fill && wk.y == 0 && warp == 0) {
+    for (int idx = lane; idx < a.nv * r; idx += 32) {
+      const int v = idx / r, s = idx - v * r;
+      out[(size_t)v * a.out_vstride + (size_t)r * a.out_rstride + s] = make_double2(0.0, 0.0);
     }
-    // generate the q tile for degrees k0 .. k0+31 at latitudes jc0 .. jc0+127
-    for (int jl = tid; jl < kAnaJC; jl += kAnaThreads) {
-      const int j = jc0 + jl;
-      if (j < P.Jh) {
-        const double mu = P.mu_n[j];
-        const double2 sd = P.ckpt[(size_t)(off + c) * P.Jh + j];
-        double qa = sd.x, qb = sd.y;
-        qs[0 * kAnaQS + jl] = qa;
-        qs[16 * kAnaQS + jl] = qb;
+  }
+  if (c * kChunk >= nout) return;
+
+  const int k0 = c * kChunk;
+  bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
+  const double2* seeds = P.ckpt + (size_t)(P.ck_off[r] + c) * P.Jh;
+  const int ncol = 2 * a.nv;
+  const int jh4 = a.xl.jh4, nc = a.xl.nc;
+  const double* xr = x + (size_t)r * jh4 * 2 * nc * 4;
+
+  double acc[2][2][NT][2];
 #pragma unroll
-        for (int kk = 2; kk < kChunk; kk += 2) {
-          qa = fma(mu, qb, -bs[kk] * qa);
-          qb = fma(mu, qa, -bs[kk + 1] * qb);
-          qs[(kk >> 1) * kAnaQS + jl] = qa;
-          qs[(16 + (kk >> 1)) * kAnaQS + jl] = qb;
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int n = 0; n < NT; ++n) { acc[p][mt][n][0] = 0.0; acc[p][mt][n][1] = 0.0; }
+
+  const int nblk = (P.Jh + 31) >> 5;
+  for (int jb32 = 0; jb32 < nblk; ++jb32) {
+    __syncwarp();
+    // regenerate q for 32 degrees at latitude jh = 32*jb32 + lane
+    const int jh = (jb32 << 5) + lane;
+    if (jh < P.Jh) {
+      const double mu = P.mu_n[jh];
+      const double2 sd = seeds[jh];
+      double qa = sd.x, qb = sd.y;
+      qs[lane] = qa;
+      qs[16 * kQS + lane] = qb;
+#pragma unroll
+      for (int kk = 2; kk < kChunk; kk += 2) {
+        qa = fma(mu, qb, -bs[kk] * qa);
+        qb = fma(mu, qa, -bs[kk + 1] * qb);
+        qs[(kk >> 1) * kQS + lane] = qa;
+        qs[(16 + (kk >> 1)) * kQS + lane] = qb;
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < kChunk; ++kk) qs[((kk & 1) * 16 + (kk >> 1)) * kQS + lane] = 0.0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int jb = (jb32 << 3) + s;
+      const bool ok = (jb * 4 + t) < P.Jh;
+      double bv[2][NT];
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const bool col = (n * 8 + g) < ncol;
+          bv[p][n] = (ok && col) ? xr[(((size_t)jb * 2 + p) * nc + n * 8) * 4 + lane] : 0.0;
         }
-      } else {
 #pragma unroll
-        for (int kk = 0; kk < kChunk; ++kk) qs[((kk & 1) * 16 + (kk >> 1)) * kAnaQS + jl] = 0.0;
-      }
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const double av = qs[(p * 16 + mt * 8 + g) * kQS + s * 4 + t];
+#pragma unroll
+          for (int n = 0; n < NT; ++n) dmma884(acc[p][mt][n], av, bv[p][n]);
+        }
     }
-    __syncthreads();
-    const double* qrow = qs + (size_t)(par * 16 + half * 8 + g) * kAnaQS + t;
-    const double* xcol = xs + (size_t)(par * kAnaJC + t) * XS + g;
-#pragma unroll 4
-    for (int j0 = 0; j0 < kAnaJC; j0 += 4) {
-      const double av = qrow[j0];
+  }
+
+  // epilogue: row k = k0 + p + 2 (8 mt + g); columns (re, im) of vector n*4 + t
+  const double* gr = P.gsc + (size_t)r * P.ldk;
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int k = k0 + p + 2 * (8 * mt + g);
+      if (k >= nout) continue;
+      const double gs = gr[k];
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
-        const double bv = xcol[(size_t)j0 * XS + n * 8];
-        dmma884(acc[n], av, bv);
+        const int v = n * 4 + t;
+        if (v < a.nv)
+          out[(size_t)v * a.out_vstride + (size_t)r * a.out_rstride + r + k] =
+              make_double2(acc[p][mt][n][0] * gs, acc[p][mt][n][1] * gs);
       }
     }
-  }
-
-  // epilogue: rows k = k0 + par + 2*(8 half + g), cols (re, im) of vector n*4 + t
-  const int k = k0 + par + 2 * (8 * half + g);
-  const int nout = a.smax - r + 1;
-  if (k < nout) {
-    const double gs = P.gsc[(size_t)r * P.ldk + k];
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      const int v = n * 4 + t;
-      if (v < a.nv) {
-        double2 val = make_double2(acc[n][0] * gs, acc[n][1] * gs);
-        a.out[(size_t)v * a.out_vstride + (size_t)r * a.out_rstride + r + k] = val;
-      }
-    }
-  }
-  if (a.zero_fill && c == 0) {
-    for (int idx = tid; idx < a.nv * r; idx += kAnaThreads) {
-      const int v = idx / r, s = idx - v * r;
-      a.out[(size_t)v * a.out_vstride + (size_t)r * a.out_rstride + s] = make_double2(0.0, 0.0);
-    }
-  }
 }
 
 template <int NT>
 int launch_ana_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st) {
-  constexpr int XS = 8 * NT + 4;
-  const size_t smem = sizeof(double) * (32 * kAnaQS + 2 * kAnaJC * XS + kChunk);
+  const size_t smem = sizeof(double) * kAnaWarps * (kChunk * kQS + kChunk);
   auto kern = ana_kernel<NT>;
-  if (smem > 48 * 1024) SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem > 48 * 1024)
+    SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   StageScope sc("legendre_analysis", st);
-  kern<<<dim3(nwork, a.nmembers), kAnaThreads, smem, st>>>(P, a);
+  kern<<<dim3(nwork, a.nmembers), kAnaWarps * 32, smem, st>>>(P, a);
   SW_LAUNCH_CHECK();
   return kOk;
 }
 
 }  // namespace
 
+int ana_warps_per_cta() { return kAnaWarps; }
+
 int launch_analysis(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st) {
   if (a.nv <= 0) return kOk;
   if (a.nv <= 4) return launch_ana_t<1>(P, a, nwork, st);
   if (a.nv <= 8) return launch_ana_t<2>(P, a, nwork, st);
+  if (a.nv <= 12) return launch_ana_t<3>(P, a, nwork, st);
   if (a.nv <= 16) return launch_ana_t<4>(P, a, nwork, st);
   set_error("analysis vectors per launch must be <= 16");
   return kUsage;

@@ -22,19 +22,20 @@ struct SynArgs {
   int nJB;                 // set by the launcher
 };
 
-// Input layout of analysis: x[v][r][jh][2] double2 = (S, D) -- the weighted
-// north+south and north-south Fourier combinations for vector v.
+// Input of analysis: the weighted north+south (S) and north-south (D) Fourier
+// combinations of nv vectors in the fragment-native XLayout (common.cuh);
+// x points at the vector group being analysed.
 struct AnaArgs {
-  const double2* x;
-  int nv;                  // number of vectors (<= 16 per launch)
+  const double* x;
+  XLayout xl;
+  int nv;                  // number of vectors in this group (<= 16)
   double2* out;            // out[v * out_vstride + r * out_rstride + s]
   long long out_vstride;
   long long out_rstride;
   int smax;                // highest degree written (R, or R+1 for the H shift)
   int zero_fill;           // also write zeros for s < r
-  const int2* work;        // (r, chunk) list, one CTA each
-  long long x_mstride;     // double2 elements between members (blockIdx.y)
-  long long out_mstride;   // complex elements between members
+  const int2* work;        // (r, first chunk) list, one CTA (ana_warps_per_cta chunks) each
+  long long out_mstride;   // complex elements between members (blockIdx.y)
   int nmembers;
 };
 
@@ -42,5 +43,6 @@ int build_checkpoints(const PlanDev& P, const double* a_tab, const double* b_tab
                       const double* sect_fac, double2* ckpt, cudaStream_t st);
 int launch_synthesis(const PlanDev& P, const SynArgs& a, int B, int mode, cudaStream_t st);
 int launch_analysis(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st);
+int ana_warps_per_cta();
 
 }  // namespace swsdc

@@ -9,7 +9,7 @@
 #include "../../paper_1805_07923_b200/csrc/fft_core.cuh"
 
 int main(int argc, char** argv) {
-  int sizes[] = {1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 13, 14, 16, 22, 24, 25, 33, 48, 50, 96, 100, 125, 143, 192, 256,
+  int sizes[] = {1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 13, 14, 16, 22, 24, 25, 32, 33, 48, 50, 64, 96, 100, 125, 128, 143, 192, 256, 2048,
                  384, 512, 768, 1920, 3840};
   double worst = 0.0;
   for (int n : sizes) {
@@ -30,20 +30,24 @@ int main(int argc, char** argv) {
       ref[k].x = (double)sr; ref[k].y = (double)si;
     }
     swfft::FftPlan p = swfft::make_fft_plan(n);
-    // forward
-    y = x;
-    swfft::fft_forward_serial(y.data(), p, tw.data());
+    // forward on a padded ring
+    std::vector<double2> buf(swfft::padded_len(n));
+    for (int i = 0; i < n; ++i) buf[swfft::pad_idx(i)] = x[i];
+    swfft::fft_forward_serial(buf.data(), p, tw.data());
     double err = 0;
     for (int k = 0; k < n; ++k) {
-      int pos = swfft::digit_rev(p, k);
-      err = fmax(err, fabs(y[pos].x - ref[k].x) + fabs(y[pos].y - ref[k].y));
+      int pos = swfft::pad_idx(swfft::digit_rev(p, k));
+      err = fmax(err, fabs(buf[pos].x - ref[k].x) + fabs(buf[pos].y - ref[k].y));
     }
     // inverse: place ref (spectrum) digit-reversed, run inverse, expect n * x
-    std::vector<double2> z(n);
-    for (int k = 0; k < n; ++k) z[swfft::digit_rev(p, k)] = ref[k];
+    std::vector<double2> z(swfft::padded_len(n));
+    for (int k = 0; k < n; ++k) z[swfft::pad_idx(swfft::digit_rev(p, k))] = ref[k];
     swfft::fft_inverse_serial(z.data(), p, tw.data());
     double err2 = 0;
-    for (int i = 0; i < n; ++i) err2 = fmax(err2, fabs(z[i].x / n - x[i].x) + fabs(z[i].y / n - x[i].y));
+    for (int i = 0; i < n; ++i) {
+      const double2 zi = z[swfft::pad_idx(i)];
+      err2 = fmax(err2, fabs(zi.x / n - x[i].x) + fabs(zi.y / n - x[i].y));
+    }
     printf("n=%5d stages=%d fwd_err=%.3e inv_err=%.3e\n", n, p.nstage, err, err2);
     worst = fmax(worst, fmax(err / sqrt((double)n), err2));
   }
