@@ -3,7 +3,7 @@
 Headline (BASELINE.json configs[1]): SH transform-pair throughput at T255 on the
 384x768 Gaussian grid, fp64, batch of 15 seeded fields (3 variables x 5 nodes);
 one step = synthesize + analyze of the batch, inputs resident in HBM, L2 flushed
-(256 MiB write) before every timed step.  `e2e` is the same metric through the
+(256 MiB write + read-back) before every timed step.  `e2e` is the same metric through the
 public API with pinned HOST buffers, H2D of the coefficients and D2H of the
 result inside every timed step.
 
@@ -237,6 +237,13 @@ def run_ours(args, world, rank, local):
     g = torch.empty((NF, I, J), dtype=torch.float64, device=dev)
     out = torch.empty_like(c)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    flush_sink = torch.empty(1, dtype=torch.float64, device=dev)
+
+    def flush_l2():
+        # write > L2, then read it back so the dirty lines are written back
+        # before the timed step (the step then starts from a cold, clean L2)
+        flush.fill_(1.0)
+        torch.sum(flush, dim=0, out=flush_sink)
 
     def step():
         plan.synthesize(c, out=g)
@@ -268,7 +275,7 @@ def run_ours(args, world, rank, local):
         l0 = _lib.launch_count()
         _lib.profile_enable(True)
         for k in range(args.steps):
-            flush.zero_()
+            flush_l2()
             starts[k].record()
             step()
             ends[k].record()
@@ -301,7 +308,7 @@ def run_ours(args, world, rank, local):
     if dist:
         dist.barrier()
     for k in range(args.steps):
-        flush.zero_()
+        flush_l2()
         e_s[k].record()
         step_e2e()
         e_e[k].record()
@@ -358,7 +365,7 @@ def run_ours(args, world, rank, local):
         "data": "synthetic (seeded spectra, amplitude (n+1)^-1.5, rms 1e3/1e-5/1e-6; SURVEY §8d)",
         "config": {"workload": WORKLOAD, "R": R, "grid": [I, J], "fields": NF,
                    "global_fields": NF * world, "parallelism": f"replicas x{world} (weak)",
-                   "l2": "flushed (256 MiB write) before every timed step"},
+                   "l2": "flushed before every timed step (256 MiB write + read-back, so no dirty lines carry over)"},
         "roofline": roof,
         "step_roofline": {"flops": pair_flops, "achieved_tflops": pair_flops / step_s / 1e12,
                           "frac_fp64": pair_flops / step_s / 1e12 / peak_fp64},

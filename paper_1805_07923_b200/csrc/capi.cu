@@ -23,8 +23,10 @@ using namespace swsdc;
 struct swsdc_plan {
   PlanDev dev{};
   std::vector<void*> owned;
-  int2* work[2] = {nullptr, nullptr};  // analysis work lists for smax = R, R + 1
-  int nwork[2] = {0, 0};
+  // analysis work lists [smax = R, R + 1][lsplit = 1, 2]: CTAs of 4/lsplit chunks
+  int2* work[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int nwork[2][2] = {{0, 0}, {0, 0}};
+  int nchunks[2] = {0, 0};
   int ldy = 0;
   char* ws = nullptr;
   size_t ws_bytes = 0;
@@ -147,6 +149,8 @@ int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, dou
             bool zero_fill, cudaStream_t st) {
   const PlanDev& P = p->dev;
   const int which = (smax == P.R) ? 0 : 1;
+  // split latitudes over 2 warps when the chunk tasks alone cannot fill the GPU
+  const int ls = ((long long)p->nchunks[which] * nmembers < 1800) ? 1 : 0;
   for (int v0 = 0; v0 < xl.nv; v0 += 16) {
     AnaArgs a{};
     a.nv = (xl.nv - v0 < 16) ? xl.nv - v0 : 16;
@@ -157,10 +161,10 @@ int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, dou
     a.out_rstride = out_rstride;
     a.smax = smax;
     a.zero_fill = zero_fill ? 1 : 0;
-    a.work = p->work[which];
+    a.work = p->work[which][ls];
     a.out_mstride = out_mstride;
     a.nmembers = nmembers;
-    SW_TRY(launch_analysis(P, a, p->nwork[which], st));
+    SW_TRY(launch_analysis(P, a, p->nwork[which][ls], ls ? 2 : 1, st));
   }
   return kOk;
 }
@@ -248,13 +252,16 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
     rs += (9 - rs % 8) % 8;  // == 1 (mod 8) double2 slots: rings differ in bank group
     P.ring_stride = rs;
   }
-  std::vector<int2> work[2];
+  std::vector<int2> work[2][2];
   for (int which = 0; which < 2; ++which) {
     const int smax = R + which;
     for (int r = 0; r <= R; ++r) {
       const int nout = smax - r + 1;
-      const int wpc = ana_warps_per_cta();
-      for (int c = 0; c * kChunk < nout; c += wpc) work[which].push_back(make_int2(r, c));
+      p->nchunks[which] += (nout + kChunk - 1) / kChunk;
+      for (int ls = 0; ls < 2; ++ls) {
+        const int cpc = ana_warps_per_cta() >> ls;  // chunks per CTA
+        for (int c = 0; c * kChunk < nout; c += cpc) work[which][ls].push_back(make_int2(r, c));
+      }
     }
   }
 
@@ -268,13 +275,14 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
       (st = upload(p, beta, &d_beta)) || (st = upload(p, gsc, &d_gsc)) ||
       (st = upload(p, eps, &d_eps)) || (st = upload(p, a, &d_a)) || (st = upload(p, b, &d_b)) ||
       (st = upload(p, sect, &d_sect)) || (st = upload(p, ck_off, &d_off)) ||
-      (st = upload(p, tw, &d_tw)) || (st = upload(p, rev, &d_rev)) || (st = upload(p, work[0], &p->work[0])) ||
-      (st = upload(p, work[1], &p->work[1]))) {
+      (st = upload(p, tw, &d_tw)) || (st = upload(p, rev, &d_rev)) ||
+      (st = upload(p, work[0][0], &p->work[0][0])) || (st = upload(p, work[0][1], &p->work[0][1])) ||
+      (st = upload(p, work[1][0], &p->work[1][0])) || (st = upload(p, work[1][1], &p->work[1][1]))) {
     swsdc_plan_destroy(p);
     return st;
   }
-  p->nwork[0] = (int)work[0].size();
-  p->nwork[1] = (int)work[1].size();
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) p->nwork[i][j] = (int)work[i][j].size();
   void* ck = nullptr;
   if (cudaMalloc(&ck, sizeof(double2) * (size_t)nck * P.Jh) != cudaSuccess) {
     set_error("cudaMalloc of the checkpoint table failed");

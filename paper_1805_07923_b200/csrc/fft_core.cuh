@@ -6,10 +6,11 @@
 // pair) are packed into one complex ring z = g_north + i g_south so a single
 // complex FFT serves both (see fourier.cu).
 //
-//   forward  : decimation in frequency, natural-order input, digit-reversed
-//              output, twiddles exp(-2 pi i e / N)
-//   inverse  : decimation in time, digit-reversed input, natural-order output,
-//              conjugate twiddles
+// Both directions run decimation in time: digit-reversed input (the loaders
+// scatter through a permutation table), natural-order output, twiddles
+// applied before each butterfly (exp(-2 pi i e / N) forward, conjugate
+// inverse).  A DIF variant (natural in, digit-reversed out) is kept for the
+// self-test.
 //
 // Stages use radix 16, 8, 4, 2, 3, 5 (register butterflies; 16 and 8 are
 // 4x4 / 2x4 decompositions with constant inner twiddles) and 7, 11, 13 via a
@@ -262,9 +263,12 @@ SW_HD void twiddles(double2* w, const double2* tw, int e1, bool inverse) {
 
 // One butterfly of stage s on a padded ring, butterfly index b in [0, n/R).
 // DIF (forward): load, DFT, twiddle, store.  DIT (inverse): load, twiddle, DFT, store.
-template <int R, bool INV>
+// DIT: twiddle-before (digit-reversed input, natural output when the stages
+// run last to first); otherwise DIF twiddle-after (natural input, digit-
+// reversed output, stages first to last).  CONJ selects exp(+2 pi i ...).
+template <int R, bool DIT, bool CONJ>
 SW_HD void stage_butterfly_t(double2* buf, const FftPlan& p, int s, int b, const double2* tw) {
-  constexpr bool inverse = INV;
+  constexpr bool inverse = CONJ;
   const int L = p.span[s];
   const int m = L / R;
   const int blk = (m == 1) ? b : (int)udiv((uint32_t)b, p.mmag[s]);
@@ -281,7 +285,7 @@ SW_HD void stage_butterfly_t(double2* buf, const FftPlan& p, int s, int b, const
       w1 = tw[e1]; w2 = tw[2 * e1]; w4 = tw[4 * e1]; w8 = tw[8 * e1];
       if (inverse) { w1.y = -w1.y; w2.y = -w2.y; w4.y = -w4.y; w8.y = -w8.y; }
     }
-    if (inverse && j != 0) {
+    if (DIT && j != 0) {
 #pragma unroll
       for (int q = 1; q < 16; ++q) {
         double2 w = (q & 1) ? w1 : mk2(1.0, 0.0);
@@ -292,7 +296,7 @@ SW_HD void stage_butterfly_t(double2* buf, const FftPlan& p, int s, int b, const
       }
     }
     small_dft<16>(v, inverse);
-    if (!inverse && j != 0) {
+    if (!DIT && j != 0) {
 #pragma unroll
       for (int q = 1; q < 16; ++q) {
         double2 w = (q & 1) ? w1 : mk2(1.0, 0.0);
@@ -308,13 +312,13 @@ SW_HD void stage_butterfly_t(double2* buf, const FftPlan& p, int s, int b, const
   }
   double2 w[R];
   if (j != 0) twiddles<R>(w, tw, j * (p.n / L), inverse);
-  if (inverse && j != 0) {
+  if (DIT && j != 0) {
 #pragma unroll
     for (int q = 1; q < R; ++q) v[q] = cmul(v[q], w[q]);
   }
   if (R == 7 || R == 11 || R == 13) prime_dft<R>(v, tw, p.n, inverse);
   else small_dft<R>(v, inverse);
-  if (!inverse && j != 0) {
+  if (!DIT && j != 0) {
 #pragma unroll
     for (int q = 1; q < R; ++q) v[q] = cmul(v[q], w[q]);
   }
@@ -324,32 +328,35 @@ SW_HD void stage_butterfly_t(double2* buf, const FftPlan& p, int s, int b, const
 
 // BIGP selects whether the rare prime radices 7, 11, 13 are compiled in (they
 // raise register pressure, so kernels are instantiated both ways).
-template <bool BIGP, bool INV>
+template <bool BIGP, bool DIT, bool CONJ>
 SW_HD void stage_butterfly(double2* buf, const FftPlan& p, int s, int b, const double2* tw) {
   switch (p.radix[s]) {
-    case 16: stage_butterfly_t<16, INV>(buf, p, s, b, tw); break;
-    case 8: stage_butterfly_t<8, INV>(buf, p, s, b, tw); break;
-    case 4: stage_butterfly_t<4, INV>(buf, p, s, b, tw); break;
-    case 2: stage_butterfly_t<2, INV>(buf, p, s, b, tw); break;
-    case 3: stage_butterfly_t<3, INV>(buf, p, s, b, tw); break;
-    case 5: stage_butterfly_t<5, INV>(buf, p, s, b, tw); break;
+    case 16: stage_butterfly_t<16, DIT, CONJ>(buf, p, s, b, tw); break;
+    case 8: stage_butterfly_t<8, DIT, CONJ>(buf, p, s, b, tw); break;
+    case 4: stage_butterfly_t<4, DIT, CONJ>(buf, p, s, b, tw); break;
+    case 2: stage_butterfly_t<2, DIT, CONJ>(buf, p, s, b, tw); break;
+    case 3: stage_butterfly_t<3, DIT, CONJ>(buf, p, s, b, tw); break;
+    case 5: stage_butterfly_t<5, DIT, CONJ>(buf, p, s, b, tw); break;
     default:
       if (BIGP) {
-        if (p.radix[s] == 7) stage_butterfly_t<7, INV>(buf, p, s, b, tw);
-        else if (p.radix[s] == 11) stage_butterfly_t<11, INV>(buf, p, s, b, tw);
-        else stage_butterfly_t<13, INV>(buf, p, s, b, tw);
+        if (p.radix[s] == 7) stage_butterfly_t<7, DIT, CONJ>(buf, p, s, b, tw);
+        else if (p.radix[s] == 11) stage_butterfly_t<11, DIT, CONJ>(buf, p, s, b, tw);
+        else stage_butterfly_t<13, DIT, CONJ>(buf, p, s, b, tw);
       }
   }
 }
 
-// Whole transform on one padded ring, sequentially (host self-test).
-inline void fft_forward_serial(double2* buf, const FftPlan& p, const double2* tw) {
+// Whole transforms on one padded ring, sequentially (host self-test).
+// DIF forward: natural in, digit-reversed out.
+inline void fft_forward_dif_serial(double2* buf, const FftPlan& p, const double2* tw) {
   for (int s = 0; s < p.nstage; ++s)
-    for (int b = 0; b < p.n / p.radix[s]; ++b) stage_butterfly<true, false>(buf, p, s, b, tw);
+    for (int b = 0; b < p.n / p.radix[s]; ++b) stage_butterfly<true, false, false>(buf, p, s, b, tw);
 }
-inline void fft_inverse_serial(double2* buf, const FftPlan& p, const double2* tw) {
+// DIT (what the kernels run): digit-reversed in, natural out; CONJ = inverse.
+template <bool CONJ>
+inline void fft_dit_serial(double2* buf, const FftPlan& p, const double2* tw) {
   for (int s = p.nstage - 1; s >= 0; --s)
-    for (int b = 0; b < p.n / p.radix[s]; ++b) stage_butterfly<true, true>(buf, p, s, b, tw);
+    for (int b = 0; b < p.n / p.radix[s]; ++b) stage_butterfly<true, true, CONJ>(buf, p, s, b, tw);
 }
 
 }  // namespace swfft

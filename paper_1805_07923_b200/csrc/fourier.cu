@@ -31,7 +31,9 @@
 namespace swsdc {
 namespace {
 
-template <bool BIGP, bool INV>
+constexpr int kSweMaxPts = 4;   // grid points per thread in the fused SWE kernel
+
+template <bool BIGP, bool CONJ>
 __device__ __forceinline__ void fft_stage_all(double2* rings, int nrings, const PlanDev& P, int s) {
   const swfft::FftPlan& fp = P.fft;
   const int r = fp.radix[s];
@@ -40,19 +42,21 @@ __device__ __forceinline__ void fft_stage_all(double2* rings, int nrings, const 
   for (int t = threadIdx.x; t < total; t += blockDim.x) {
     const int q = (nb == 1) ? t : (int)swfft::udiv((uint32_t)t, fp.bmag[s]);
     const int b = t - q * nb;
-    swfft::stage_butterfly<BIGP, INV>(rings + (size_t)q * P.ring_stride, fp, s, b, P.tw);
+    swfft::stage_butterfly<BIGP, true, CONJ>(rings + (size_t)q * P.ring_stride, fp, s, b, P.tw);
   }
 }
 
-// Forward: natural -> digit-reversed.  Caller synchronises before.
+// Both directions are decimation in time: input in digit-reversed slots
+// (P.rev), output in natural order.  Caller synchronises before.
+// Forward: exp(-2 pi i k n / I).
 template <bool BIGP>
 __device__ void fft_forward(double2* rings, int nrings, const PlanDev& P) {
-  for (int s = 0; s < P.fft.nstage; ++s) {
+  for (int s = P.fft.nstage - 1; s >= 0; --s) {
     fft_stage_all<BIGP, false>(rings, nrings, P, s);
     __syncthreads();
   }
 }
-// Inverse (unnormalised): digit-reversed -> natural.
+// Inverse (unnormalised): exp(+2 pi i k n / I).
 template <bool BIGP>
 __device__ void fft_inverse(double2* rings, int nrings, const PlanDev& P) {
   for (int s = P.fft.nstage - 1; s >= 0; --s) {
@@ -82,42 +86,60 @@ __device__ __forceinline__ void pair_spectrum(double2 E, double2 O, int r, doubl
 
 // Fill nr rings (ring q of CTA-local pair i at rings[(q*np + i) * RS]) from
 // (E, O) rows eo[q][r][jh0 + i]; every slot is written (zeros off-band).
+// Loads are issued kU at a time before use so each thread keeps several
+// global reads in flight.
 __device__ __forceinline__ void fill_rings(double2* rings, const PlanDev& P, const double2* eo,
                                            size_t fstride, int nr, int np, int lnp, int jh0) {
+  constexpr int kU = 4;
   const int R = P.R, I = P.I, RS = P.ring_stride;
   const int nband = (nr * (R + 1)) << lnp;
   const int nmid = I - 2 * R - 1;
   const int nzero = (nr * nmid) << lnp;
-  for (int idx = threadIdx.x; idx < nband + nzero; idx += blockDim.x) {
-    if (idx < nband) {
-      const int i = idx & (np - 1);
-      const int qr = idx >> lnp;
-      const int q = qr / (R + 1), r = qr - q * (R + 1);
-      const int jh = jh0 + i;
-      double2* ring = rings + (size_t)(q * np + i) * RS;
-      double2 zp = d2(0.0, 0.0), zm = zp;
-      if (jh < P.Jh) {
-        const double2* src = eo + q * fstride + ((size_t)r * P.Jh + jh) * 2;
-        pair_spectrum(src[0], src[1], r, zp, zm);
+  const int nt = blockDim.x;
+  for (int base = threadIdx.x; base < nband; base += kU * nt) {
+    double2 E[kU], O[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int idx = base + u * nt;
+      E[u] = O[u] = d2(0.0, 0.0);
+      if (idx < nband) {
+        const int i = idx & (np - 1), qr = idx >> lnp;
+        const int q = qr / (R + 1), r = qr - q * (R + 1);
+        if (jh0 + i < P.Jh) {
+          const double2* src = eo + q * fstride + ((size_t)r * P.Jh + jh0 + i) * 2;
+          E[u] = src[0];
+          O[u] = src[1];
+        }
       }
-      ring[P.rev[r]] = zp;
-      if (r != 0) ring[P.rev[I - r]] = zm;
-    } else {
-      const int z = idx - nband;
-      const int i = z & (np - 1);
-      const int qk = z >> lnp;
-      const int q = qk / nmid, k = R + 1 + (qk - q * nmid);
-      rings[(size_t)(q * np + i) * RS + P.rev[k]] = d2(0.0, 0.0);
     }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int idx = base + u * nt;
+      if (idx < nband) {
+        const int i = idx & (np - 1), qr = idx >> lnp;
+        const int q = qr / (R + 1), r = qr - q * (R + 1);
+        double2 zp, zm;
+        pair_spectrum(E[u], O[u], r, zp, zm);
+        double2* ring = rings + (size_t)(q * np + i) * RS;
+        ring[P.rev[r]] = zp;
+        if (r != 0) ring[P.rev[I - r]] = zm;
+      }
+    }
+  }
+  for (int z = threadIdx.x; z < nzero; z += nt) {
+    const int i = z & (np - 1);
+    const int qk = z >> lnp;
+    const int q = qk / nmid, k = R + 1 + (qk - q * nmid);
+    rings[(size_t)(q * np + i) * RS + P.rev[k]] = d2(0.0, 0.0);
   }
 }
 
 // Unpack F_n, F_s (already divided by n_lon) at wavenumber r from a forward-
-// transformed packed ring.
+// transformed packed ring (natural order).
 __device__ __forceinline__ void get_pair(const double2* ring, const PlanDev& P, int r, double2& Fn,
                                          double2& Fs) {
-  const double2 zk = ring[P.rev[r]];
-  const double2 zm = ring[P.rev[r == 0 ? 0 : P.I - r]];
+  const double2 zk = ring[swfft::pad_idx(r)];
+  const double2 zm = ring[swfft::pad_idx(r == 0 ? 0 : P.I - r)];
   const double h = 0.5 / P.I;
   Fn = d2((zk.x + zm.x) * h, (zk.y - zm.y) * h);
   Fs = d2((zk.y + zm.y) * h, (zm.x - zk.x) * h);
@@ -181,17 +203,37 @@ __global__ void __launch_bounds__(256, 2) g2f_kernel(PlanDev P, const double* gr
   const int jh0 = blockIdx.x * np;
   const double* gin[2] = {grid + (size_t)f * grid_fstride,
                           (MODE == 0 ? grid : grid2) + (size_t)f * grid_fstride};
-  for (int idx = threadIdx.x; idx < NIN * (P.I << lnp); idx += blockDim.x) {
-    const int q = (NIN == 1) ? 0 : idx / (P.I << lnp);
-    const int rem = idx - q * (P.I << lnp);
-    const int il = rem >> lnp, i = rem & (np - 1);
-    const int jh = jh0 + i;
-    double2 z = d2(0.0, 0.0);
-    if (jh < P.Jh) {
-      const double* gq = gin[q] + (size_t)il * P.J;
-      z = d2(gq[jn_of(P, jh)], gq[js_of(P, jh)]);
+  {
+    constexpr int kU = 4;
+    const int ntot = NIN * (P.I << lnp), nt = blockDim.x;
+    for (int base = threadIdx.x; base < ntot; base += kU * nt) {
+      double2 z[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int idx = base + u * nt;
+        z[u] = d2(0.0, 0.0);
+        if (idx < ntot) {
+          const int q = (NIN == 1) ? 0 : idx / (P.I << lnp);
+          const int rem = idx - q * (P.I << lnp);
+          const int il = rem >> lnp, i = rem & (np - 1);
+          const int jh = jh0 + i;
+          if (jh < P.Jh) {
+            const double* gq = gin[q] + (size_t)il * P.J;
+            z[u] = d2(gq[jn_of(P, jh)], gq[js_of(P, jh)]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int idx = base + u * nt;
+        if (idx < ntot) {
+          const int q = (NIN == 1) ? 0 : idx / (P.I << lnp);
+          const int rem = idx - q * (P.I << lnp);
+          const int il = rem >> lnp, i = rem & (np - 1);
+          rings[(size_t)(q * np + i) * P.ring_stride + P.rev[il]] = z[u];
+        }
+      }
     }
-    rings[(size_t)(q * np + i) * P.ring_stride + swfft::pad_idx(il)] = z;
   }
   __syncthreads();
   fft_forward<BIGP>(rings, NIN * np, P);
@@ -245,14 +287,30 @@ __global__ void __launch_bounds__(256, 2) swe_grid_kernel(PlanDev P, const doubl
   const double fn = 2.0 * omega * mu;         // f = 2 Omega mu (swe.py:178); south: -fn
   const double c2o = 2.0 * omega / radius;    // swe.py:179
   const double ic2 = 1.0 / (1.0 - mu * mu);   // swe.py:180
-  for (int il = threadIdx.x; il < P.I; il += blockDim.x) {
-    const int p = swfft::pad_idx(il);
-    const double2 U = rings[p], V = rings[RS + p], Z = rings[2 * RS + p], D = rings[3 * RS + p];
+  // the forward FFT wants its input in digit-reversed slots: read every grid
+  // point this thread owns, barrier, then write the products permuted
+  double2 gv[kSweMaxPts][NIN];
+#pragma unroll
+  for (int u = 0; u < kSweMaxPts; ++u) {
+    const int il = threadIdx.x + u * blockDim.x;
+    if (il < P.I) {
+      const int p = swfft::pad_idx(il);
+#pragma unroll
+      for (int q = 0; q < NIN; ++q) gv[u][q] = rings[q * RS + p];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kSweMaxPts; ++u) {
+    const int il = threadIdx.x + u * blockDim.x;
+    if (il >= P.I) continue;
+    const int p = P.rev[il];
+    const double2 U = gv[u][0], V = gv[u][1], Z = gv[u][2], D = gv[u][3];
     // swe.py:262,265 : tend_zeta grid = -f delta - (2 Omega/a) V ; tend_delta grid = f zeta - (2 Omega/a) U
     rings[p] = d2(-fn * D.x - c2o * V.x, fn * D.y - c2o * V.y);
     rings[RS + p] = d2(fn * Z.x - c2o * U.x, -fn * Z.y - c2o * U.y);
     if (NONLIN) {
-      const double2 Ph = rings[4 * RS + p];
+      const double2 Ph = gv[u][NIN - 1];
       // swe.py:271-273 : Phi U, Phi V, zeta U, zeta V, KE = (U^2 + V^2) / (2 (1 - mu^2))
       rings[2 * RS + p] = d2(Ph.x * U.x, Ph.y * U.y);
       rings[3 * RS + p] = d2(Ph.x * V.x, Ph.y * V.y);
@@ -365,8 +423,14 @@ int swe_launch(const PlanDev& P, const double2* eo, long long eo_mstride, double
   const size_t smem = sizeof(double2) * nr * P.ring_stride;
   dim3 gridDim(P.Jh, nmembers);
   SW_TRY(set_smem((const void*)swe_grid_kernel<NONLIN, BIGP>, smem));
+  int threads = pick_threads(nr * max_butterflies(P), BIGP);
+  while (threads * kSweMaxPts < P.I && threads < 256) threads *= 2;
+  if (threads * kSweMaxPts < P.I) {
+    set_error("n_lon too large for the fused grid kernel");
+    return kUsage;
+  }
   StageScope sc("swe_grid", st);
-  swe_grid_kernel<NONLIN, BIGP><<<gridDim, pick_threads(nr * max_butterflies(P), BIGP), smem, st>>>(
+  swe_grid_kernel<NONLIN, BIGP><<<gridDim, threads, smem, st>>>(
       P, eo, eo_mstride, x, xl, omega, radius);
   SW_LAUNCH_CHECK();
   return kOk;

@@ -96,79 +96,63 @@ __device__ __forceinline__ double2 fetch_coef(const double2* f, int srcR, int r,
   return f[(size_t)r * (srcR + 1) + s];
 }
 
-// d_t = (t+2) eps_{t+1} c_{t+1} - (t-1) eps_t c_{t-1}: H-synthesis folded onto P.
-__device__ __forceinline__ double2 h_fold(const double2* f, int srcR, int r, int t,
-                                          const double* eps_r, double scale_hi, double scale_lo) {
-  const double2 hi = fetch_coef(f, srcR, r, t + 1);
-  const double2 lo = fetch_coef(f, srcR, r, t - 1);
-  const double ch = (t + 2.0) * eps_r[t + 1] * scale_hi;
-  const double cl = (t - 1.0) * eps_r[t] * scale_lo;
-  return make_double2(ch * hi.x - cl * lo.x, ch * hi.y - cl * lo.y);
-}
-
 __device__ __forceinline__ double inv_lap(int s, double radius) {
   if (s <= 0) return 0.0;
   const double lam = (-(double)s * (s + 1.0)) / (radius * radius);
   return 1.0 / lam;
 }
 
-// Coefficient of synthesis field b at (r, s) for the kernel mode (unscaled).
-template <int MODE>
-__device__ __forceinline__ double2 syn_coef(const PlanDev& P, const SynArgs& a, int b, int r, int s) {
-  const double* eps_r = P.eps + (size_t)r * P.ldk;
-  if (MODE == kSynPlain) return fetch_coef(a.src + (size_t)b * a.src_fstride, a.src_R, r, s);
-  if (MODE == kSynUV) {
-    // U = i r chi - d(psi),  V = i r psi + d(chi)   (spharm.py:272-278)
-    const double2* psi = a.src;
-    const double2* chi = a.src2;
-    const double2 c = fetch_coef(b == 0 ? chi : psi, a.src_R, r, s);
-    const double2 h = h_fold(b == 0 ? psi : chi, a.src_R, r, s, eps_r, 1.0, 1.0);
-    const double sg = (b == 0) ? -1.0 : 1.0;
-    return make_double2(-r * c.y + sg * h.x, r * c.x + sg * h.y);
-  }
-  // kSynSWE: state (phi, zeta, delta) -> U/a, V/a, zeta, delta, phi
-  const double2* phi = a.src;
-  const double2* zeta = a.src + a.src_fstride;
-  const double2* delta = a.src + 2 * a.src_fstride;
-  if (b < 2) {
-    // psi = invlap(zeta), chi = invlap(delta) (swe.py:186-187), then 1/a (swe.py:189)
-    const double ia = 1.0 / a.radius;
-    const double2 cm = fetch_coef(b == 0 ? delta : zeta, a.src_R, r, s);
-    const double sm = inv_lap(s, a.radius) * ia;
-    const double2 hh = h_fold(b == 0 ? zeta : delta, a.src_R, r, s, eps_r,
-                              inv_lap(s + 1, a.radius) * ia, inv_lap(s - 1, a.radius) * ia);
-    const double sg = (b == 0) ? -1.0 : 1.0;
-    return make_double2(-r * cm.y * sm + sg * hh.x, r * cm.x * sm + sg * hh.y);
-  }
-  return fetch_coef(b == 2 ? zeta : (b == 3 ? delta : phi), a.src_R, r, s);
-}
-
-// Per-lane registers of one chunk in flight.
-template <int B>
+// Raw per-lane loads of one chunk (degree s = r + k0 + lane) kept in registers
+// while the previous chunk computes; all arithmetic on them is deferred to
+// stage_chunk so the loads stay in flight.
+//   plain: c_b(s) for B fields
+//   UV   : psi, chi at s, s+1, s-1
+//   SWE  : zeta, delta at s, s+1, s-1 and phi' at s
+template <int B, int MODE>
 struct ChunkRegs {
-  double2 coef[B];   // degree k0 + lane
-  double2 coef_x;    // degree k0 + 32 + lane (lanes 0, 1)
-  double beta, beta_x;
+  static constexpr int NRAW = MODE == kSynPlain ? B : (MODE == kSynUV ? 6 : 7);
+  double2 raw[NRAW];
+  double eps0, eps1, g;    // eps_s, eps_{s+1}, chunk scale g
+  double beta, beta_x;     // beta[k0 + lane], beta[k0 + 32 + lane] (lanes 0, 1)
   double2 seed[kSynNL];
 };
 
 template <int B, int MODE>
-__device__ __forceinline__ void load_chunk(ChunkRegs<B>& c, const PlanDev& P, const SynArgs& a,
+__device__ __forceinline__ void load_chunk(ChunkRegs<B, MODE>& c, const PlanDev& P, const SynArgs& a,
                                            int r, int ci, int nstep, int lane, const int* jh) {
   const int k0 = ci * kChunk;
-  const double* g_r = P.gsc + (size_t)r * P.ldk;
+  const int k = k0 + lane, s = r + k;
   const double* b_r = P.beta + (size_t)r * P.ldk;
-  const int k = k0 + lane;
-  const double g = g_r[k];
+  const double* e_r = P.eps + (size_t)r * P.ldk;
+  c.g = P.gsc[(size_t)r * P.ldk + k];
+  c.eps0 = e_r[s];
+  c.eps1 = e_r[s + 1];
+  if (MODE == kSynPlain) {
 #pragma unroll
-  for (int b = 0; b < B; ++b) {
-    double2 v = make_double2(0.0, 0.0);
-    if (k < nstep) {
-      v = syn_coef<MODE>(P, a, b, r, r + k);
-      v.x *= g;
-      v.y *= g;
-    }
-    c.coef[b] = v;
+    for (int b = 0; b < B; ++b) c.raw[b] = fetch_coef(a.src + (size_t)b * a.src_fstride, a.src_R, r, s);
+  } else if (MODE == kSynUV) {
+    const double2* f0 = a.src;   // psi
+    const double2* f1 = a.src2;  // chi
+    c.raw[0] = fetch_coef(f0, a.src_R, r, s);
+    c.raw[1] = fetch_coef(f1, a.src_R, r, s);
+    c.raw[2] = fetch_coef(f0, a.src_R, r, s + 1);
+    c.raw[3] = fetch_coef(f0, a.src_R, r, s - 1);
+    c.raw[4] = fetch_coef(f1, a.src_R, r, s + 1);
+    c.raw[5] = fetch_coef(f1, a.src_R, r, s - 1);
+  } else {
+    const double2* zeta = a.src + a.src_fstride;
+    const double2* delta = a.src + 2 * a.src_fstride;
+    c.raw[0] = fetch_coef(zeta, a.src_R, r, s);
+    c.raw[1] = fetch_coef(delta, a.src_R, r, s);
+    c.raw[2] = fetch_coef(zeta, a.src_R, r, s + 1);
+    c.raw[3] = fetch_coef(zeta, a.src_R, r, s - 1);
+    c.raw[4] = fetch_coef(delta, a.src_R, r, s + 1);
+    c.raw[5] = fetch_coef(delta, a.src_R, r, s - 1);
+    c.raw[6] = fetch_coef(a.src, a.src_R, r, s);
+  }
+  if (k >= nstep) {
+#pragma unroll
+    for (int q = 0; q < ChunkRegs<B, MODE>::NRAW; ++q) c.raw[q] = make_double2(0.0, 0.0);
   }
   c.beta = b_r[k];
   c.beta_x = (lane < 2) ? b_r[k + kChunk] : 0.0;
@@ -176,6 +160,48 @@ __device__ __forceinline__ void load_chunk(ChunkRegs<B>& c, const PlanDev& P, co
 #pragma unroll
   for (int l = 0; l < kSynNL; ++l)
     c.seed[l] = (jh[l] < P.Jh) ? P.ckpt[(size_t)off * P.Jh + jh[l]] : make_double2(0.0, 0.0);
+}
+
+// d_t = (t+2) eps_{t+1} c_{t+1} - (t-1) eps_t c_{t-1}: H-synthesis folded onto P.
+__device__ __forceinline__ double2 hfold(double2 hi, double2 lo, double e0, double e1, int t,
+                                         double shi, double slo) {
+  const double ch = (t + 2.0) * e1 * shi, cl = (t - 1.0) * e0 * slo;
+  return make_double2(ch * hi.x - cl * lo.x, ch * hi.y - cl * lo.y);
+}
+
+// Coefficients of the B synthesis fields at degree s = r + k0 + lane, scaled
+// by g, written to the warp's slab cs[b][lane].
+template <int B, int MODE>
+__device__ __forceinline__ void stage_chunk(const ChunkRegs<B, MODE>& c, double2* cs, int r,
+                                            int s, double radius, int lane) {
+  double2 v[B];
+  if (MODE == kSynPlain) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) v[b] = c.raw[b];
+  } else if (MODE == kSynUV) {
+    // U = i r chi - d(psi),  V = i r psi + d(chi)   (spharm.py:272-278)
+    const double2 hp = hfold(c.raw[2], c.raw[3], c.eps0, c.eps1, s, 1.0, 1.0);
+    const double2 hc = hfold(c.raw[4], c.raw[5], c.eps0, c.eps1, s, 1.0, 1.0);
+    v[0] = make_double2(-r * c.raw[1].y - hp.x, r * c.raw[1].x - hp.y);
+    v[1] = make_double2(-r * c.raw[0].y + hc.x, r * c.raw[0].x + hc.y);
+  } else {
+    // psi = invlap(zeta), chi = invlap(delta) (swe.py:186-187), then 1/a (swe.py:189)
+    const double ia = 1.0 / radius;
+    const double s0 = inv_lap(s, radius) * ia, sp = inv_lap(s + 1, radius) * ia,
+                 sm = inv_lap(s - 1, radius) * ia;
+    const double2 hpsi = hfold(c.raw[2], c.raw[3], c.eps0, c.eps1, s, sp, sm);
+    const double2 hchi = hfold(c.raw[4], c.raw[5], c.eps0, c.eps1, s, sp, sm);
+    v[0] = make_double2(-r * c.raw[1].y * s0 - hpsi.x, r * c.raw[1].x * s0 - hpsi.y);  // U/a
+    v[1] = make_double2(-r * c.raw[0].y * s0 + hchi.x, r * c.raw[0].x * s0 + hchi.y);  // V/a
+    v[2] = c.raw[0];
+    v[3] = c.raw[1];
+    v[4] = c.raw[6];
+  }
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    cs[b * kCS + lane] = make_double2(v[b].x * c.g, v[b].y * c.g);
+    if (lane < 2) cs[b * kCS + kChunk + lane] = make_double2(0.0, 0.0);
+  }
 }
 
 template <int B>
@@ -254,15 +280,11 @@ syn_kernel(PlanDev P, SynArgs a) {
     const int r = rows[ir], nstep = nst[ir];
     const int c0 = (NSPLIT == 1) ? 0 : cb, c1 = (NSPLIT == 1) ? nch[ir] : ce;
     if (c0 < c1) {
-      ChunkRegs<B> nx;
+      ChunkRegs<B, MODE> nx;
       load_chunk<B, MODE>(nx, P, a, r, c0, nstep, lane, jh);
       for (int ci = c0; ci < c1; ++ci) {
         __syncwarp();
-#pragma unroll
-        for (int b = 0; b < B; ++b) {
-          cs[b * kCS + lane] = nx.coef[b];
-          if (lane < 2) cs[b * kCS + kChunk + lane] = make_double2(0.0, 0.0);
-        }
+        stage_chunk<B, MODE>(nx, cs, r, r + ci * kChunk + lane, a.radius, lane);
         bs[lane] = nx.beta;
         if (lane < 2) bs[kChunk + lane] = nx.beta_x;
         double qa[kSynNL], qb[kSynNL];
@@ -410,7 +432,24 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// B fragments (S and D parity) of latitude block jb for the NT n-tiles.
 template <int NT>
+__device__ __forceinline__ void load_b(double (&bv)[2][NT], const double* xr, int jb, int Jh,
+                                       int nc, int ncol, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  const bool ok = (jb * 4 + t) < Jh;
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const bool col = (n * 8 + g) < ncol;
+      bv[p][n] = (ok && col) ? xr[(((size_t)jb * 2 + p) * nc + n * 8) * 4 + lane] : 0.0;
+    }
+}
+
+// LSPLIT warps share one chunk, each taking every LSPLIT-th latitude block;
+// their accumulators are reduced through shared memory in warp order.
+template <int NT, int LSPLIT>
 __global__ void __launch_bounds__(kAnaWarps * 32)
 ana_kernel(PlanDev P, AnaArgs a) {
   extern __shared__ __align__(16) double smem[];
@@ -422,7 +461,7 @@ ana_kernel(PlanDev P, AnaArgs a) {
   const double* x = a.x + (size_t)blockIdx.y * a.xl.mstride;
   double2* out = a.out + (size_t)blockIdx.y * a.out_mstride;
   const int2 wk = a.work[blockIdx.x];
-  const int r = wk.x, c = wk.y + warp;
+  const int r = wk.x, c = wk.y + warp / LSPLIT, half = warp % LSPLIT;
   const int nout = a.smax - r + 1;
 
   if (a.zero_fill && wk.y == 0 && warp == 0) {
@@ -431,14 +470,7 @@ ana_kernel(PlanDev P, AnaArgs a) {
       out[(size_t)v * a.out_vstride + (size_t)r * a.out_rstride + s] = make_double2(0.0, 0.0);
     }
   }
-  if (c * kChunk >= nout) return;
-
-  const int k0 = c * kChunk;
-  bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
-  const double2* seeds = P.ckpt + (size_t)(P.ck_off[r] + c) * P.Jh;
-  const int ncol = 2 * a.nv;
-  const int jh4 = a.xl.jh4, nc = a.xl.nc;
-  const double* xr = x + (size_t)r * jh4 * 2 * nc * 4;
+  const bool active = c * kChunk < nout;
 
   double acc[2][2][NT][2];
 #pragma unroll
@@ -448,50 +480,94 @@ ana_kernel(PlanDev P, AnaArgs a) {
 #pragma unroll
       for (int n = 0; n < NT; ++n) { acc[p][mt][n][0] = 0.0; acc[p][mt][n][1] = 0.0; }
 
-  const int nblk = (P.Jh + 31) >> 5;
-  for (int jb32 = 0; jb32 < nblk; ++jb32) {
-    __syncwarp();
-    // regenerate q for 32 degrees at latitude jh = 32*jb32 + lane
-    const int jh = (jb32 << 5) + lane;
-    if (jh < P.Jh) {
-      const double mu = P.mu_n[jh];
-      const double2 sd = seeds[jh];
-      double qa = sd.x, qb = sd.y;
-      qs[lane] = qa;
-      qs[16 * kQS + lane] = qb;
+  const int k0 = c * kChunk;
+  if (active) {
+    bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
+    const double2* seeds = P.ckpt + (size_t)(P.ck_off[r] + c) * P.Jh;
+    const int ncol = 2 * a.nv;
+    const int nc = a.xl.nc;
+    const double* xr = x + (size_t)r * a.xl.jh4 * 2 * nc * 4;
+    const int nblk = (P.Jh + 31) >> 5;
+    double bcur[2][NT];
+    if (half < nblk) load_b<NT>(bcur, xr, half << 3, P.Jh, nc, ncol, lane);
+    for (int jb32 = half; jb32 < nblk; jb32 += LSPLIT) {
+      __syncwarp();
+      // regenerate q for 32 degrees at latitude jh = 32*jb32 + lane
+      const int jh = (jb32 << 5) + lane;
+      if (jh < P.Jh) {
+        const double mu = P.mu_n[jh];
+        const double2 sd = seeds[jh];
+        double qa = sd.x, qb = sd.y;
+        qs[lane] = qa;
+        qs[16 * kQS + lane] = qb;
 #pragma unroll
-      for (int kk = 2; kk < kChunk; kk += 2) {
-        qa = fma(mu, qb, -bs[kk] * qa);
-        qb = fma(mu, qa, -bs[kk + 1] * qb);
-        qs[(kk >> 1) * kQS + lane] = qa;
-        qs[(16 + (kk >> 1)) * kQS + lane] = qb;
+        for (int kk = 2; kk < kChunk; kk += 2) {
+          qa = fma(mu, qb, -bs[kk] * qa);
+          qb = fma(mu, qa, -bs[kk + 1] * qb);
+          qs[(kk >> 1) * kQS + lane] = qa;
+          qs[(16 + (kk >> 1)) * kQS + lane] = qb;
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < kChunk; ++kk) qs[((kk & 1) * 16 + (kk >> 1)) * kQS + lane] = 0.0;
       }
-    } else {
+      __syncwarp();
 #pragma unroll
-      for (int kk = 0; kk < kChunk; ++kk) qs[((kk & 1) * 16 + (kk >> 1)) * kQS + lane] = 0.0;
+      for (int s = 0; s < 8; ++s) {
+        // prefetch the next k-step's B fragments (the next block's first
+        // k-step is fetched across the generation phase)
+        double bnx[2][NT];
+        const int jnext = (s < 7) ? (jb32 << 3) + s + 1 : ((jb32 + LSPLIT) << 3);
+        if (s < 7 || jb32 + LSPLIT < nblk) load_b<NT>(bnx, xr, jnext, P.Jh, nc, ncol, lane);
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const double av = qs[(p * 16 + mt * 8 + g) * kQS + s * 4 + t];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) dmma884(acc[p][mt][n], av, bcur[p][n]);
+          }
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+          for (int n = 0; n < NT; ++n) bcur[p][n] = bnx[p][n];
+      }
     }
-    __syncwarp();
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int jb = (jb32 << 3) + s;
-      const bool ok = (jb * 4 + t) < P.Jh;
-      double bv[2][NT];
+  }
+
+  if (LSPLIT > 1) {
+    // warps half > 0 hand their partial sums to the half-0 warp of their chunk
+    __syncthreads();
+    double* red = smem + (size_t)warp * (kChunk * kQS + kChunk);
+    if (half > 0 && active) {
 #pragma unroll
       for (int p = 0; p < 2; ++p)
 #pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          const bool col = (n * 8 + g) < ncol;
-          bv[p][n] = (ok && col) ? xr[(((size_t)jb * 2 + p) * nc + n * 8) * 4 + lane] : 0.0;
-        }
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            const int e = ((p * 2 + mt) * NT + n) * 2;
+            red[e * 32 + lane] = acc[p][mt][n][0];
+            red[(e + 1) * 32 + lane] = acc[p][mt][n][1];
+          }
+    }
+    __syncthreads();
+    if (half > 0 || !active) return;
+    for (int h = 1; h < LSPLIT; ++h) {
+      const double* src = smem + (size_t)(warp + h) * (kChunk * kQS + kChunk);
 #pragma unroll
       for (int p = 0; p < 2; ++p)
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          const double av = qs[(p * 16 + mt * 8 + g) * kQS + s * 4 + t];
+        for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-          for (int n = 0; n < NT; ++n) dmma884(acc[p][mt][n], av, bv[p][n]);
-        }
+          for (int n = 0; n < NT; ++n) {
+            const int e = ((p * 2 + mt) * NT + n) * 2;
+            acc[p][mt][n][0] += src[e * 32 + lane];
+            acc[p][mt][n][1] += src[(e + 1) * 32 + lane];
+          }
     }
+  } else if (!active) {
+    return;
   }
 
   // epilogue: row k = k0 + p + 2 (8 mt + g); columns (re, im) of vector n*4 + t
@@ -513,10 +589,10 @@ ana_kernel(PlanDev P, AnaArgs a) {
     }
 }
 
-template <int NT>
+template <int NT, int LSPLIT>
 int launch_ana_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st) {
   const size_t smem = sizeof(double) * kAnaWarps * (kChunk * kQS + kChunk);
-  auto kern = ana_kernel<NT>;
+  auto kern = ana_kernel<NT, LSPLIT>;
   if (smem > 48 * 1024)
     SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   StageScope sc("legendre_analysis", st);
@@ -525,16 +601,23 @@ int launch_ana_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st)
   return kOk;
 }
 
+template <int NT>
+int launch_ana_nt(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, cudaStream_t st) {
+  if (lsplit == 2) return launch_ana_t<NT, 2>(P, a, nwork, st);
+  return launch_ana_t<NT, 1>(P, a, nwork, st);
+}
+
 }  // namespace
 
 int ana_warps_per_cta() { return kAnaWarps; }
 
-int launch_analysis(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st) {
+// a.work must list CTAs of kAnaWarps / lsplit consecutive chunks.
+int launch_analysis(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, cudaStream_t st) {
   if (a.nv <= 0) return kOk;
-  if (a.nv <= 4) return launch_ana_t<1>(P, a, nwork, st);
-  if (a.nv <= 8) return launch_ana_t<2>(P, a, nwork, st);
-  if (a.nv <= 12) return launch_ana_t<3>(P, a, nwork, st);
-  if (a.nv <= 16) return launch_ana_t<4>(P, a, nwork, st);
+  if (a.nv <= 4) return launch_ana_nt<1>(P, a, nwork, lsplit, st);
+  if (a.nv <= 8) return launch_ana_nt<2>(P, a, nwork, lsplit, st);
+  if (a.nv <= 12) return launch_ana_nt<3>(P, a, nwork, lsplit, st);
+  if (a.nv <= 16) return launch_ana_nt<4>(P, a, nwork, lsplit, st);
   set_error("analysis vectors per launch must be <= 16");
   return kUsage;
 }

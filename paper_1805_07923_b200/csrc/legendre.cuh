@@ -42,7 +42,7 @@ struct AnaArgs {
 int build_checkpoints(const PlanDev& P, const double* a_tab, const double* b_tab,
                       const double* sect_fac, double2* ckpt, cudaStream_t st);
 int launch_synthesis(const PlanDev& P, const SynArgs& a, int B, int mode, cudaStream_t st);
-int launch_analysis(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st);
+int launch_analysis(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, cudaStream_t st);
 int ana_warps_per_cta();
 
 }  // namespace swsdc

@@ -33,16 +33,24 @@ int main(int argc, char** argv) {
     // forward on a padded ring
     std::vector<double2> buf(swfft::padded_len(n));
     for (int i = 0; i < n; ++i) buf[swfft::pad_idx(i)] = x[i];
-    swfft::fft_forward_serial(buf.data(), p, tw.data());
+    swfft::fft_forward_dif_serial(buf.data(), p, tw.data());
     double err = 0;
     for (int k = 0; k < n; ++k) {
       int pos = swfft::pad_idx(swfft::digit_rev(p, k));
       err = fmax(err, fabs(buf[pos].x - ref[k].x) + fabs(buf[pos].y - ref[k].y));
     }
+    // forward DIT (kernel path): digit-reversed input, natural output
+    std::vector<double2> d(swfft::padded_len(n));
+    for (int i = 0; i < n; ++i) d[swfft::pad_idx(swfft::digit_rev(p, i))] = x[i];
+    swfft::fft_dit_serial<false>(d.data(), p, tw.data());
+    for (int k = 0; k < n; ++k) {
+      const double2 dk = d[swfft::pad_idx(k)];
+      err = fmax(err, fabs(dk.x - ref[k].x) + fabs(dk.y - ref[k].y));
+    }
     // inverse: place ref (spectrum) digit-reversed, run inverse, expect n * x
     std::vector<double2> z(swfft::padded_len(n));
     for (int k = 0; k < n; ++k) z[swfft::pad_idx(swfft::digit_rev(p, k))] = ref[k];
-    swfft::fft_inverse_serial(z.data(), p, tw.data());
+    swfft::fft_dit_serial<true>(z.data(), p, tw.data());
     double err2 = 0;
     for (int i = 0; i < n; ++i) {
       const double2 zi = z[swfft::pad_idx(i)];
