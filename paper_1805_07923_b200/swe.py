@@ -48,6 +48,8 @@ def combine(weights, tensors, out: torch.Tensor | None = None) -> torch.Tensor:
     (sdc.py:211-220).  All tensors share shape and dtype complex128."""
     pairs = [(float(w), t) for w, t in zip(weights, tensors) if float(w) != 0.0]
     ref = tensors[0]
+    if any(t.shape != ref.shape for t in tensors):
+        raise ValueError("combine needs tensors of one shape")
     if out is None:
         out = torch.empty_like(ref)
     if not pairs:
