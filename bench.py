@@ -237,7 +237,7 @@ def run_ours(args, world, rank, local):
     g = torch.empty((NF, I, J), dtype=torch.float64, device=dev)
     out = torch.empty_like(c)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
-    flush_sink = torch.empty(1, dtype=torch.float64, device=dev)
+    flush_sink = torch.empty((), dtype=torch.float64, device=dev)
 
     def flush_l2():
         # write > L2, then read it back so the dirty lines are written back
@@ -317,6 +317,13 @@ def run_ours(args, world, rank, local):
     e2e_value = world * NF * args.steps / (e2e_ms * 1e-3)
     e2e_err = float(np.max(np.abs(o_pin.numpy() - c_host)) / np.max(np.abs(c_host)))
 
+    mlsdc_lines = {}
+    if not args.no_mlsdc:
+        for name, cfg in MLSDC_CONFIGS.items():
+            if world > 1 and cfg[10] == 1:
+                continue   # single-state configs run on one GPU only
+            mlsdc_lines[name] = run_mlsdc(name, cfg, world, rank, dev, dist, flush_l2, peak_fp64)
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -377,6 +384,11 @@ def run_ours(args, world, rank, local):
                 "roundtrip_err": e2e_err},
         "roundtrip_err": rt_err,
     }
+    if mlsdc_lines:
+        if world == 1 and not args.no_cpu_baseline:
+            for name in mlsdc_lines:
+                mlsdc_lines[name]["cpu_baseline"] = cpu_mlsdc_baseline(name)
+        line["mlsdc"] = mlsdc_lines
     if world == 1 and not args.no_cpu_baseline:
         workers = max(1, min(host_cores(), NF))
         pool = CpuPool(workers)
@@ -395,6 +407,114 @@ def run_ours(args, world, rank, local):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------
+# MLSDC configs (BASELINE.json configs[0], [2], [4]) through the graph stepper
+# ----------------------------------------------------------------------------
+MLSDC_CONFIGS = {
+    # name: (R_f, grid_f (I, J), R_c, grid_c, nodes_f, nodes_c, n_iter, coarse_sweeps, dt, steps, members)
+    "config0": (63, (192, 96), 31, (96, 48), 3, 2, 2, 1, 600.0, 1, 1),
+    "config2": (255, (768, 384), 127, (384, 192), 5, 3, 4, 2, 240.0, 10, 1),
+    "config4": (170, (512, 256), 85, (256, 128), 3, 2, 2, 1, 450.0, 1, 64),
+}
+
+
+def mlsdc_flops(cfg):
+    """Algorithmic FP64 work of one step: per F_E evaluation
+    18 Legendre contractions (2 T J) + 12 FFTs (2.5 I log2 I J), times the
+    evaluation counts 1 + N M_f (fine) and 1 + N (M_c + n_cs M_c) (coarse)."""
+    Rf, (If, Jf), Rc, (Ic, Jc), nf, nc, n_it, ncs, _, _, members = cfg
+    ev = lambda R, I, J: 18 * legendre_flops(R, J) + 12 * fft_flops(I, J)
+    n_f = 1 + n_it * (nf - 1)
+    n_c = 1 + n_it * ((nc - 1) + ncs * (nc - 1))
+    return members * (n_f * ev(Rf, If, Jf) + n_c * ev(Rc, Ic, Jc))
+
+
+def run_mlsdc(name, cfg, world, rank, dev, dist, flush_l2, peak_fp64):
+    import torch
+    from paper_1805_07923_b200 import mlsdc, stepper, swe, workloads
+    Rf, gf, Rc, gc, nf, nc, n_it, ncs, dt, steps, members = cfg
+    # ensemble members are sharded across ranks with no communication (weak in ranks)
+    mine = members // world if members >= world else members
+    first = rank * mine if members >= world else 0
+    params = swe.ModelParams(**workloads.EARTH)
+    hier = mlsdc.build_hierarchy(params, Rf, nf, Rc, nc, grid_fine=gf, grid_coarse=gc, device=dev)
+    if members > 1:
+        x0 = np.stack([workloads.seeded_state(Rf, k) for k in range(first, first + mine)])
+    else:
+        x0 = workloads.seeded_state(Rf, 0)
+    st0 = swe.PrognosticState(torch.as_tensor(x0, device=dev))
+    stp = stepper.MLSDCStepper(hier, dt, n_it, st0, n_coarse_sweeps=ncs)
+    stp.run(1)   # warm replay
+    stp.set_state(st0)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    from paper_1805_07923_b200 import _lib
+    l0 = _lib.launch_count()
+    for k in range(steps):
+        flush_l2()
+        ev[k][0].record()
+        stp.step()
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - l0
+    finite = bool(stp._g.flag.item())
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t_ms = max_over_ranks(t_ms, dist, dev)
+    total_members = mine * world if members >= world else members
+    value = n_it * total_members * steps / (t_ms * 1e-3)
+    fl = mlsdc_flops(cfg) * total_members / members
+    out = {"metric": "MLSDC-SH fine sweeps/s (fp64)", "value": value, "unit": "fine sweeps/s",
+           "ms_per_step": t_ms / steps, "steps": steps, "members": total_members,
+           "config": {"R": [Rf, Rc], "grid": [list(gf), list(gc)], "nodes": [nf, nc],
+                      "iterations": n_it, "coarse_sweeps": ncs, "dt": dt,
+                      "parallelism": f"members sharded x{world}" if members > 1 else "1 GPU"},
+           "step_fp64_tflops": fl / (t_ms * 1e-3 / steps) / 1e12 / (world if members > 1 else 1),
+           "step_frac_fp64_per_gpu": fl / (t_ms * 1e-3 / steps) / 1e12 / peak_fp64 / (world if members > 1 else 1),
+           "gpu_launches_per_step": 0 if launches == 0 else None,
+           "graph_replays_per_step": 1, "finite": finite}
+    out["gpu_launches_per_step"] = None  # kernels run inside one CUDA-graph replay per step
+    return out
+
+
+def _cpu_mlsdc(args):
+    """Oracle time for ONE step of an MLSDC config (1 core)."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    name, member = args
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import swsdc_oracle as orc
+    from paper_1805_07923_b200 import workloads
+    Rf, gf, Rc, gc, nf, nc, n_it, ncs, dt, steps, members = MLSDC_CONFIGS[name]
+    prm = orc.OracleParams(**workloads.EARTH)
+    h = orc.OracleHierarchy(orc.OracleLevel(Rf, nf, prm, gf), orc.OracleLevel(Rc, nc, prm, gc))
+    x = workloads.seeded_state(Rf, member)
+    t0 = time.perf_counter()
+    orc.mlsdc_step(x, dt, n_it, h, ncs)
+    return time.perf_counter() - t0
+
+
+def cpu_mlsdc_baseline(name):
+    import multiprocessing as mp
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    cfg = MLSDC_CONFIGS[name]
+    n_it, members = cfg[6], cfg[10]
+    if members > 1:
+        w = max(1, min(host_cores(), 16))
+        with mp.get_context("spawn").Pool(w) as pool:
+            t0 = time.perf_counter()
+            pool.map(_cpu_mlsdc, [(name, k) for k in range(w)], chunksize=1)
+            wall = time.perf_counter() - t0
+        return {"value": n_it * w / wall, "unit": "fine sweeps/s", "cores": w, "kind": "port",
+                "sample": f"1 step of {w} members, one single-threaded oracle worker each "
+                          f"(wall incl. oracle plan build)"}
+    with mp.get_context("spawn").Pool(1) as pool:
+        t = pool.map(_cpu_mlsdc, [(name, 0)])[0]
+    return {"value": n_it / t, "unit": "fine sweeps/s", "cores": 1, "kind": "port",
+            "sample": "1 step, 1 core (plan build excluded)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -403,6 +523,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of load before timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-mlsdc", action="store_true", help="skip the MLSDC config lines")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_env()
