@@ -80,6 +80,17 @@ int swsdc_solve_implicit(int truncation, const swsdc_params* params, double beta
  * (sdc._combine sdc.py:211-220 and PrognosticState algebra swe.py:77-102). */
 int swsdc_combine(int n, const double* const* x, const double* w, long long count, double* out,
                   void* stream);
+/* out = sum_k w[k] * resize(x[k], r_in[k] -> r_out) over `nmat` spectral matrices per input,
+ * n <= 32: restriction (Lagrange rows + truncate, mlsdc.py:83-88), interpolation (pad +
+ * Lagrange rows, mlsdc.py:90-95) and the FAS combination (mlsdc.py:113-124) in one launch. */
+int swsdc_spec_combine(int n, const double* const* x, const double* w, const int* r_in, int r_out,
+                       long long nmat, double* out, void* stream);
+/* One SDC node update (sdc.py:196-206): b = sum_k w[k] x[k] (states at truncation R),
+ * theta = solve_implicit(b, beta) (implicit.py:31-49), f_i = eval_f_i(theta)
+ * (swe.py:206-217), for `batch` states.  Same status rules as swsdc_solve_implicit. */
+int swsdc_sweep_node(int truncation, const swsdc_params* params, double beta, int n,
+                     const double* const* x, const double* w, int batch, double* theta,
+                     double* f_i, void* stream);
 /* spharm.truncate / spharm.pad (spharm.py:331-349) over `nmat` (R+1)^2 matrices. */
 int swsdc_resize(const double* in, int r_in, double* out, int r_out, long long nmat, void* stream);
 

@@ -1,6 +1,7 @@
 // C ABI (include/swsdc_b200.h): plan construction and the host-side
 // orchestration of the kernels for each reference entry point.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -200,7 +201,10 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
   P.J = n_lat;
   P.Jh = (n_lat + 1) / 2;
   P.ldk = ((R + 2 + kChunk + 16) + 7) / 8 * 8;
-  P.fft = swfft::make_fft_plan(n_lon);
+  {
+    const char* mr = getenv("SWSDC_FFT_MAX_RADIX");   // tuning knob (16 default, 8)
+    P.fft = swfft::make_fft_plan(n_lon, mr ? atoi(mr) : 16);
+  }
   p->ldy = R + 2;
   const int ldk = P.ldk;
 
@@ -486,6 +490,54 @@ int swsdc_combine(int n, const double* const* x, const double* w, long long coun
   }
   if (count == 0) return kOk;
   return launch_combine(a, count, S(stream));
+}
+
+int swsdc_spec_combine(int n, const double* const* x, const double* w, const int* r_in, int r_out,
+                       long long nmat, double* out, void* stream) {
+  if (n < 0 || n > kMaxCombine || nmat < 0 || r_out < 0) {
+    set_error("spec_combine takes 0..32 inputs");
+    return kUsage;
+  }
+  SpecCombineArgs a{};
+  a.n = n;
+  a.rout = r_out;
+  a.out = reinterpret_cast<double2*>(out);
+  for (int k = 0; k < n; ++k) {
+    if (r_in[k] < 0) { set_error("bad input truncation"); return kUsage; }
+    a.x[k] = reinterpret_cast<const double2*>(x[k]);
+    a.w[k] = w[k];
+    a.rin[k] = r_in[k];
+  }
+  if (nmat == 0) return kOk;
+  return launch_spec_combine(a, nmat, S(stream));
+}
+
+int swsdc_sweep_node(int R, const swsdc_params* q, double beta, int n, const double* const* x,
+                     const double* w, int batch, double* theta, double* f_i, void* stream) {
+  SW_TRY(check_params(q));
+  if (beta < 0) { set_error("implicit step must be non-negative"); return kUsage; }
+  if (R < 0 || batch < 0 || n < 0 || n > kMaxCombine) { set_error("bad arguments"); return kUsage; }
+  const ModelConsts c = consts(q);
+  for (int s = 0; s <= R; ++s) {
+    const double lam = (-(double)s * (s + 1.0)) / (c.radius * c.radius);
+    const double d = 1.0 - beta * c.nu * lam;
+    const double det = d * d - beta * beta * lam * c.phi_bar;
+    if (!(det > 0.0)) {
+      set_error("implicit system is singular; invalid model parameters");
+      return kNumerical;
+    }
+  }
+  SpecCombineArgs a{};
+  a.n = n;
+  a.rout = R;
+  for (int k = 0; k < n; ++k) {
+    a.x[k] = reinterpret_cast<const double2*>(x[k]);
+    a.w[k] = w[k];
+    a.rin[k] = R;
+  }
+  if (batch == 0) return kOk;
+  return launch_sweep_node(R, c, beta, a, reinterpret_cast<double2*>(theta),
+                           reinterpret_cast<double2*>(f_i), batch, S(stream));
 }
 
 int swsdc_resize(const double* in, int r_in, double* out, int r_out, long long nmat, void* stream) {

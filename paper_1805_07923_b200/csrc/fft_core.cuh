@@ -63,12 +63,13 @@ inline uint32_t magic_for(uint32_t d) {
 
 // Factor n into stage radices: 16s, then one 8/4/2 for the remaining power of
 // two, then 3, 5, 7, 11, 13.
-inline FftPlan make_fft_plan(int n) {
+inline FftPlan make_fft_plan(int n, int max_radix = 16) {
   FftPlan p{};
   p.n = n;
   int m = n, k = 0;
   int rad[64];
-  while (m % 16 == 0) { rad[k++] = 16; m /= 16; }
+  while (max_radix >= 16 && m % 16 == 0) { rad[k++] = 16; m /= 16; }
+  while (max_radix == 8 && m % 8 == 0) { rad[k++] = 8; m /= 8; }
   if (m % 8 == 0) { rad[k++] = 8; m /= 8; }
   if (m % 4 == 0) { rad[k++] = 4; m /= 4; }
   if (m % 2 == 0) { rad[k++] = 2; m /= 2; }

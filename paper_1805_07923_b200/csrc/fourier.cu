@@ -90,7 +90,7 @@ __device__ __forceinline__ void pair_spectrum(double2 E, double2 O, int r, doubl
 // global reads in flight.
 __device__ __forceinline__ void fill_rings(double2* rings, const PlanDev& P, const double2* eo,
                                            size_t fstride, int nr, int np, int lnp, int jh0) {
-  constexpr int kU = 4;
+  constexpr int kU = 8;
   const int R = P.R, I = P.I, RS = P.ring_stride;
   const int nband = (nr * (R + 1)) << lnp;
   const int nmid = I - 2 * R - 1;

@@ -119,7 +119,8 @@ struct ChunkRegs {
 
 template <int B, int MODE>
 __device__ __forceinline__ void load_chunk(ChunkRegs<B, MODE>& c, const PlanDev& P, const SynArgs& a,
-                                           int r, int ci, int nstep, int lane, const int* jh) {
+                                           int r, int ci, int nstep, int lane, const int* jh,
+                                           int off_r) {
   const int k0 = ci * kChunk;
   const int k = k0 + lane, s = r + k;
   const double* b_r = P.beta + (size_t)r * P.ldk;
@@ -150,13 +151,11 @@ __device__ __forceinline__ void load_chunk(ChunkRegs<B, MODE>& c, const PlanDev&
     c.raw[5] = fetch_coef(delta, a.src_R, r, s - 1);
     c.raw[6] = fetch_coef(a.src, a.src_R, r, s);
   }
-  if (k >= nstep) {
-#pragma unroll
-    for (int q = 0; q < ChunkRegs<B, MODE>::NRAW; ++q) c.raw[q] = make_double2(0.0, 0.0);
-  }
+  // degrees past the row end need no masking: fetch_coef returns 0 for s > R_in
+  (void)nstep;
   c.beta = b_r[k];
   c.beta_x = (lane < 2) ? b_r[k + kChunk] : 0.0;
-  const int off = P.ck_off[r] + ci;
+  const int off = off_r + ci;
 #pragma unroll
   for (int l = 0; l < kSynNL; ++l)
     c.seed[l] = (jh[l] < P.Jh) ? P.ckpt[(size_t)off * P.Jh + jh[l]] : make_double2(0.0, 0.0);
@@ -280,8 +279,9 @@ syn_kernel(PlanDev P, SynArgs a) {
     const int r = rows[ir], nstep = nst[ir];
     const int c0 = (NSPLIT == 1) ? 0 : cb, c1 = (NSPLIT == 1) ? nch[ir] : ce;
     if (c0 < c1) {
+      const int off_r = P.ck_off[r];
       ChunkRegs<B, MODE> nx;
-      load_chunk<B, MODE>(nx, P, a, r, c0, nstep, lane, jh);
+      load_chunk<B, MODE>(nx, P, a, r, c0, nstep, lane, jh, off_r);
       for (int ci = c0; ci < c1; ++ci) {
         __syncwarp();
         stage_chunk<B, MODE>(nx, cs, r, r + ci * kChunk + lane, a.radius, lane);
@@ -291,7 +291,7 @@ syn_kernel(PlanDev P, SynArgs a) {
 #pragma unroll
         for (int l = 0; l < kSynNL; ++l) { qa[l] = nx.seed[l].x; qb[l] = nx.seed[l].y; }
         __syncwarp();
-        if (ci + 1 < c1) load_chunk<B, MODE>(nx, P, a, r, ci + 1, nstep, lane, jh);
+        if (ci + 1 < c1) load_chunk<B, MODE>(nx, P, a, r, ci + 1, nstep, lane, jh, off_r);
         const int kn = min(kChunk, nstep - ci * kChunk);
 #pragma unroll 2
         for (int kk = 0; kk < kn; kk += 2) {
@@ -490,13 +490,24 @@ ana_kernel(PlanDev P, AnaArgs a) {
     const int nblk = (P.Jh + 31) >> 5;
     double bcur[2][NT];
     if (half < nblk) load_b<NT>(bcur, xr, half << 3, P.Jh, nc, ncol, lane);
+    // seed and mu of this lane's latitude in the next block, fetched one block ahead
+    double2 sd_nx = make_double2(0.0, 0.0);
+    double mu_nx = 0.0;
+    {
+      const int jh0 = (half << 5) + lane;
+      if (jh0 < P.Jh) { sd_nx = seeds[jh0]; mu_nx = P.mu_n[jh0]; }
+    }
     for (int jb32 = half; jb32 < nblk; jb32 += LSPLIT) {
       __syncwarp();
       // regenerate q for 32 degrees at latitude jh = 32*jb32 + lane
       const int jh = (jb32 << 5) + lane;
+      const double2 sd = sd_nx;
+      const double mu = mu_nx;
+      {
+        const int jn = ((jb32 + LSPLIT) << 5) + lane;
+        if (jn < P.Jh) { sd_nx = seeds[jn]; mu_nx = P.mu_n[jn]; }
+      }
       if (jh < P.Jh) {
-        const double mu = P.mu_n[jh];
-        const double2 sd = seeds[jh];
         double qa = sd.x, qb = sd.y;
         qs[lane] = qa;
         qs[16 * kQS + lane] = qb;

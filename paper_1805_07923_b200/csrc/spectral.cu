@@ -166,6 +166,68 @@ __global__ void resize_kernel(const double2* in, int rin, double2* out, int rout
   }
 }
 
+__global__ void spec_combine_kernel(SpecCombineArgs a, long long nmat) {
+  const int ro = a.rout;
+  const long long plane = (long long)(ro + 1) * (ro + 1);
+  const long long total = nmat * plane;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long m = idx / plane;
+    const int rs = (int)(idx - m * plane);
+    const int r = rs / (ro + 1), s = rs - r * (ro + 1);
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < a.n; ++k) {
+      const int ri = a.rin[k];
+      if (r <= ri && s <= ri) {
+        const double2 v = a.x[k][m * (long long)(ri + 1) * (ri + 1) + (long long)r * (ri + 1) + s];
+        acc.x = fma(a.w[k], v.x, acc.x);
+        acc.y = fma(a.w[k], v.y, acc.y);
+      }
+    }
+    a.out[idx] = acc;
+  }
+}
+
+// b = sum_k w_k x_k -> theta = (I - beta F_I)^-1 b -> fi = L_G(theta)
+__global__ void sweep_node_kernel(int R, ModelConsts c, double beta, SpecCombineArgs a,
+                                  double2* theta, double2* fi, long long nstates) {
+  const long long plane = (long long)(R + 1) * (R + 1);
+  const long long total = nstates * plane;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long m = idx / plane;
+    const int rs = (int)(idx - m * plane);
+    const int s = rs % (R + 1);
+    const long long o = m * 3 * plane + rs;
+    double2 b[3];
+#pragma unroll
+    for (int f = 0; f < 3; ++f) b[f] = make_double2(0.0, 0.0);
+    for (int k = 0; k < a.n; ++k) {
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        const double2 v = a.x[k][o + f * plane];
+        b[f].x = fma(a.w[k], v.x, b[f].x);
+        b[f].y = fma(a.w[k], v.y, b[f].y);
+      }
+    }
+    const double lam = lam_of(s, c.radius);
+    const double d = 1.0 - beta * c.nu * lam;
+    const double det = d * d - beta * beta * lam * c.phi_bar;
+    const double id = 1.0 / det;
+    const double bp = beta * c.phi_bar, bl = beta * lam;
+    const double2 ph = make_double2((d * b[0].x - bp * b[2].x) * id, (d * b[0].y - bp * b[2].y) * id);
+    const double2 ze = make_double2(b[1].x / d, b[1].y / d);
+    const double2 de = make_double2((d * b[2].x - bl * b[0].x) * id, (d * b[2].y - bl * b[0].y) * id);
+    theta[o] = ph;
+    theta[o + plane] = ze;
+    theta[o + 2 * plane] = de;
+    const double nl = c.nu * lam;
+    fi[o] = make_double2(-c.phi_bar * de.x + nl * ph.x, -c.phi_bar * de.y + nl * ph.y);
+    fi[o + plane] = make_double2(nl * ze.x, nl * ze.y);
+    fi[o + 2 * plane] = make_double2(-lam * ph.x + nl * de.x, -lam * ph.y + nl * de.y);
+  }
+}
+
 int grid_for(long long n, int threads) {
   long long b = (n + threads - 1) / threads;
   if (b > 148 * 16) b = 148 * 16;
@@ -217,6 +279,23 @@ int launch_solve(int R, const ModelConsts& c, double beta, const double2* b, dou
 int launch_combine(const CombineArgs& a, long long count, cudaStream_t st) {
   StageScope sc("combine", st);
   combine_kernel<<<grid_for(count, 256), 256, 0, st>>>(a, count);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_spec_combine(const SpecCombineArgs& a, long long nmat, cudaStream_t st) {
+  const long long n = nmat * (a.rout + 1) * (a.rout + 1);
+  StageScope sc("spec_combine", st);
+  spec_combine_kernel<<<grid_for(n, 256), 256, 0, st>>>(a, nmat);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_sweep_node(int R, const ModelConsts& c, double beta, const SpecCombineArgs& a,
+                      double2* theta, double2* fi, long long nstates, cudaStream_t st) {
+  const long long n = nstates * (R + 1) * (R + 1);
+  StageScope sc("sweep_node", st);
+  sweep_node_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, beta, a, theta, fi, nstates);
   SW_LAUNCH_CHECK();
   return kOk;
 }

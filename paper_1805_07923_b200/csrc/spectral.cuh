@@ -26,6 +26,22 @@ int launch_eval_fi(int R, const ModelConsts& c, const double2* x, double2* out, 
 int launch_solve(int R, const ModelConsts& c, double beta, const double2* b, double2* out,
                  long long nmat, cudaStream_t st);
 int launch_combine(const CombineArgs& a, long long count, cudaStream_t st);
+
+// Weighted sum of spectral states with per-input truncation, written at
+// truncation rout (zero-padded / truncated): out = sum_k w_k resize(x_k).
+struct SpecCombineArgs {
+  const double2* x[kMaxCombine];
+  double w[kMaxCombine];
+  int rin[kMaxCombine];
+  int n;
+  double2* out;
+  int rout;
+};
+int launch_spec_combine(const SpecCombineArgs& a, long long nmat, cudaStream_t st);
+// One sweep node (sdc.py:196-206 fused): b = sum_k w_k x_k (all at R);
+// theta = solve(b, beta); fi = L_G(theta).  nstates = states per input.
+int launch_sweep_node(int R, const ModelConsts& c, double beta, const SpecCombineArgs& a,
+                      double2* theta, double2* fi, long long nstates, cudaStream_t st);
 int launch_resize(const double2* in, int rin, double2* out, int rout, long long nmat,
                   cudaStream_t st);
 

@@ -67,6 +67,33 @@ def combine(weights, tensors, out: torch.Tensor | None = None) -> torch.Tensor:
     return out
 
 
+def spec_combine(weights, tensors, r_out: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out = sum_k w_k resize(x_k -> r_out), one launch; inputs may have
+    different truncations (last two dims) but the same leading shape.
+    Exactly-zero weights are skipped (sdc.py:211-220)."""
+    pairs = [(float(w), t) for w, t in zip(weights, tensors) if float(w) != 0.0]
+    ref = tensors[0]
+    lead = tuple(ref.shape[:-2])
+    if any(tuple(t.shape[:-2]) != lead for t in tensors):
+        raise ValueError("spec_combine needs one leading shape")
+    if out is None:
+        out = torch.empty(lead + (r_out + 1, r_out + 1), dtype=torch.complex128, device=ref.device)
+    if not pairs:
+        out.zero_()
+        return out
+    if len(pairs) > 32:
+        raise ValueError("spec_combine supports at most 32 weighted terms")
+    n = len(pairs)
+    ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() for _, t in pairs])
+    ws = (ctypes.c_double * n)(*[w for w, _ in pairs])
+    rin = (ctypes.c_int * n)(*[t.shape[-1] - 1 for _, t in pairs])
+    nmat = int(np.prod(lead)) if lead else 1
+    with torch.cuda.device(ref.device):
+        _lib.check(_lib.load().swsdc_spec_combine(n, ptrs, ws, rin, r_out, nmat, _ptr(out),
+                                                  _stream_ptr(ref.device)))
+    return out
+
+
 class PrognosticState:
     """Spectral state (phi_prime, zeta, delta) at one truncation (swe.py:44-125)."""
 
@@ -282,6 +309,30 @@ class ShallowWaterRHS:
         """Fused F_E = L_F + N (swe.py:251-279) on the GPU."""
         self.counters.explicit_evals += 1
         return self._fe(state, self.include_nonlinear)
+
+    def solve_and_eval_fi(self, weights, tensors, beta: float):
+        """Fused sweep node (sdc.py:196-205): b = sum_k w_k x_k, theta = solve(b, beta),
+        f_i = F_I(theta) in ONE kernel.  Counts one solve and one implicit
+        evaluation, like the reference's solve_implicit + eval_f_i."""
+        if beta < 0:
+            raise ValueError("implicit step must be non-negative")
+        pairs = [(float(w), t) for w, t in zip(weights, tensors) if float(w) != 0.0]
+        if len(pairs) > 32:
+            raise ValueError("at most 32 terms")
+        ref = tensors[0]
+        theta = torch.empty_like(ref)
+        fi = torch.empty_like(ref)
+        n = len(pairs)
+        ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() for _, t in pairs])
+        ws = (ctypes.c_double * n)(*[w for w, _ in pairs])
+        nmat = int(np.prod(ref.shape[:-3])) if ref.dim() > 3 else 1
+        with torch.cuda.device(ref.device):
+            _lib.check(_lib.load().swsdc_sweep_node(self.truncation, ctypes.byref(self._cparams),
+                                                    float(beta), n, ptrs, ws, nmat, _ptr(theta),
+                                                    _ptr(fi), _stream_ptr(ref.device)))
+        self.counters.solves += 1
+        self.counters.implicit_evals += 1
+        return PrognosticState.from_tensor(theta), PrognosticState.from_tensor(fi)
 
     def solve_implicit(self, b: PrognosticState, beta: float) -> PrognosticState:
         """swe.py:281-288."""
