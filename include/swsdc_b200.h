@@ -48,6 +48,9 @@ const char* swsdc_version(void);
 int swsdc_plan_create(int truncation, int n_lon, int n_lat, const double* mu, const double* w,
                       swsdc_plan** out);
 int swsdc_plan_destroy(swsdc_plan* plan);
+/* Plan options: key 1 = force the large-n_lon F_E path (grids through HBM) even when the
+ * fused shared-memory grid kernel fits (used by the tests to check both paths). */
+int swsdc_plan_config(swsdc_plan* plan, int key, int value);
 /* Pre-size the scratch workspace for up to `fields` simultaneous fields (so no
  * allocation happens later, e.g. during CUDA graph capture). */
 int swsdc_plan_reserve(swsdc_plan* plan, int fields);

@@ -37,6 +37,7 @@ _SIGNATURES = {
     "swsdc_plan_create": ([_I, _I, _I, _P, _P, ctypes.POINTER(_P)], _I),
     "swsdc_plan_destroy": ([_P], _I),
     "swsdc_plan_reserve": ([_P, _I], _I),
+    "swsdc_plan_config": ([_P, _I, _I], _I),
     "swsdc_synthesize": ([_P, _P, _I, _I, _P, _P], _I),
     "swsdc_analyze": ([_P, _P, _I, _P, _P], _I),
     "swsdc_synthesize_uv": ([_P, _P, _P, _I, _I, _P, _P, _P], _I),

@@ -31,6 +31,9 @@ struct swsdc_plan {
   int ldy = 0;
   char* ws = nullptr;
   size_t ws_bytes = 0;
+  void* grid_ws = nullptr;      // large-n_lon F_E path: 5 grids per state
+  size_t grid_bytes = 0;
+  bool force_split = false;     // option 1: use the large-n_lon F_E path even when it fits
 };
 
 namespace {
@@ -321,12 +324,30 @@ int swsdc_plan_destroy(swsdc_plan* p) {
   cudaDeviceSynchronize();
   for (void* ptr : p->owned) cudaFree(ptr);
   if (p->ws) cudaFree(p->ws);
+  if (p->grid_ws) cudaFree(p->grid_ws);
   delete p;
   return kOk;
 }
 
+int swsdc_plan_config(swsdc_plan* p, int key, int value) {
+  if (!p) { set_error("plan is NULL"); return kUsage; }
+  if (key == 1) { p->force_split = value != 0; return kOk; }
+  set_error("unknown plan option");
+  return kUsage;
+}
+
 int swsdc_plan_reserve(swsdc_plan* p, int fields) {
   if (!p || fields < 0) { set_error("bad arguments"); return kUsage; }
+  if (!swe_grid_fits(p->dev) || p->force_split) {
+    const size_t need = sizeof(double) * (size_t)p->dev.I * p->dev.J * fields;
+    if (need > p->grid_bytes) {
+      if (p->grid_ws) { SW_CUDA(cudaDeviceSynchronize()); SW_CUDA(cudaFree(p->grid_ws)); }
+      p->grid_ws = nullptr;
+      p->grid_bytes = 0;
+      SW_CUDA(cudaMalloc(&p->grid_ws, need));
+      p->grid_bytes = need;
+    }
+  }
   return ensure_ws(p, 5 * fields, x_bytes_for(p, 7, fields) + x_bytes_for(p, fields, 1),
                    7 * fields);
 }
@@ -438,7 +459,29 @@ int swsdc_eval_fe(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, c
   a.eo_mstride = 5 * fstride;
   a.nmembers = batch;
   SW_TRY(launch_synthesis(P, a, 5, kSynSWE, S(stream)));
-  SW_TRY(launch_swe_grid(P, nl, eo, 5 * fstride, x, xl, batch, q->omega, q->radius, S(stream)));
+  if (swe_grid_fits(P) && !p->force_split) {
+    SW_TRY(launch_swe_grid(P, nl, eo, 5 * fstride, x, xl, batch, q->omega, q->radius, S(stream)));
+  } else {
+    // large n_lon: grids through HBM (p->grid_ws), products transformed pairwise
+    const long long gfield = (long long)P.I * P.J;
+    const size_t need = sizeof(double) * (size_t)gfield * 5 * batch;
+    if (need > p->grid_bytes) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(S(stream), &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+        set_error("grid workspace too small during stream capture");
+        return kUsage;
+      }
+      if (p->grid_ws) { SW_CUDA(cudaDeviceSynchronize()); SW_CUDA(cudaFree(p->grid_ws)); }
+      p->grid_ws = nullptr;
+      p->grid_bytes = 0;
+      SW_CUDA(cudaMalloc(&p->grid_ws, need));
+      p->grid_bytes = need;
+    }
+    double* g = reinterpret_cast<double*>(p->grid_ws);
+    SW_TRY(launch_fourier_to_grid(P, eo, fstride, g, gfield, 5 * batch, S(stream)));
+    SW_TRY(launch_swe_products(P, nl, g, gfield, 5 * gfield, x, xl, batch, q->omega, q->radius,
+                               S(stream)));
+  }
   const long long yv = (long long)(P.R + 1) * p->ldy;
   SW_TRY(ana_run(p, x, xl, batch, y, yv, p->ldy, nv * yv, P.R + 1, false, S(stream)));
   return launch_finalize_swe(P, y, nv * yv, p->ldy, reinterpret_cast<double2*>(out), 3 * plane, nl,

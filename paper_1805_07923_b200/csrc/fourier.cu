@@ -356,6 +356,90 @@ __global__ void __launch_bounds__(256, 2) swe_grid_kernel(PlanDev P, const doubl
   }
 }
 
+// ---------------------------------------------------------------------------
+// Large-n_lon variant of the fused grid stage: the 5 grids (U/a, V/a, zeta,
+// delta, phi') come from HBM (written by f2g_kernel) and the 7 products are
+// transformed pairwise through 2 rings, each pair completing its analysis
+// vectors: (A1, ZU) -> v1, v6; (A2, ZV) -> v2, v5; (PU, PV) -> v0, v4; KE -> v3.
+// ---------------------------------------------------------------------------
+template <bool NONLIN, bool BIGP>
+__global__ void __launch_bounds__(256, 1) swe_prod_kernel(PlanDev P, const double* grids,
+                                                          long long gfield, long long gmember,
+                                                          double* x, XLayout xl, double omega,
+                                                          double radius) {
+  extern __shared__ __align__(16) double2 rings[];  // [2][RS]
+  const int jh = blockIdx.x, m = blockIdx.y;
+  const int RS = P.ring_stride, I = P.I;
+  const int jn = jn_of(P, jh), js = js_of(P, jh);
+  const bool eq = (jn == js);
+  const double* gm = grids + (size_t)m * gmember;
+  const double mu = P.mu_n[jh];
+  const double fn = 2.0 * omega * mu, c2o = 2.0 * omega / radius, ic2 = 1.0 / (1.0 - mu * mu);
+  const double w = P.w_n[jh], wc = w * ic2, ia = 1.0 / radius;
+  double* xm = x + (size_t)m * xl.mstride;
+  // grid value of field q at longitude il, north (x) and south (y)
+  auto gv = [&](int q, int il) {
+    const double* g = gm + (size_t)q * gfield + (size_t)il * P.J;
+    return d2(g[jn], g[js]);
+  };
+  // linear only (include_nonlinear=False): one pass of (A1, A2) -> v0, v1
+  for (int pass = NONLIN ? 0 : 4; pass < (NONLIN ? 4 : 5); ++pass) {
+    const int nr = (pass == 3) ? 1 : 2;
+    for (int il = threadIdx.x; il < I; il += blockDim.x) {
+      const double2 U = gv(0, il), V = gv(1, il);
+      double2 a, b = d2(0.0, 0.0);
+      if (pass == 0) {          // A1 = -f delta - c2o V ; ZU = zeta U
+        const double2 D = gv(3, il), Z = gv(2, il);
+        a = d2(-fn * D.x - c2o * V.x, fn * D.y - c2o * V.y);
+        b = d2(Z.x * U.x, Z.y * U.y);
+      } else if (pass == 1) {   // A2 = f zeta - c2o U ; ZV = zeta V
+        const double2 Z = gv(2, il);
+        a = d2(fn * Z.x - c2o * U.x, -fn * Z.y - c2o * U.y);
+        b = d2(Z.x * V.x, Z.y * V.y);
+      } else if (pass == 2) {   // PU = phi U ; PV = phi V
+        const double2 Ph = gv(4, il);
+        a = d2(Ph.x * U.x, Ph.y * U.y);
+        b = d2(Ph.x * V.x, Ph.y * V.y);
+      } else if (pass == 4) {   // linear: A1, A2
+        const double2 D = gv(3, il), Z = gv(2, il);
+        a = d2(-fn * D.x - c2o * V.x, fn * D.y - c2o * V.y);
+        b = d2(fn * Z.x - c2o * U.x, -fn * Z.y - c2o * U.y);
+      } else {                  // KE = (U^2 + V^2) / (2 (1 - mu^2))
+        a = d2(0.5 * (U.x * U.x + V.x * V.x) * ic2, 0.5 * (U.y * U.y + V.y * V.y) * ic2);
+      }
+      const int p = P.rev[il];
+      rings[p] = a;
+      if (nr == 2) rings[RS + p] = b;
+    }
+    __syncthreads();
+    fft_forward<BIGP>(rings, nr, P);
+    for (int r = threadIdx.x; r <= P.R; r += blockDim.x) {
+      double2 An, As, Bn = d2(0.0, 0.0), Bs = Bn;
+      get_pair(rings, P, r, An, As);
+      if (nr == 2) get_pair(rings + RS, P, r, Bn, Bs);
+      const double rwa = r * wc * ia, wa = wc * ia;
+      if (pass == 0) {
+        put_x(xm, xl, 1, r, jh, cadd2(cscale(An, w), ir_scale(Bn, -rwa)),
+              cadd2(cscale(As, w), ir_scale(Bs, -rwa)), eq);
+        put_x(xm, xl, 6, r, jh, cscale(Bn, wa), cscale(Bs, wa), eq);
+      } else if (pass == 1) {
+        put_x(xm, xl, 2, r, jh, cadd2(cscale(An, w), ir_scale(Bn, rwa)),
+              cadd2(cscale(As, w), ir_scale(Bs, rwa)), eq);
+        put_x(xm, xl, 5, r, jh, cscale(Bn, wa), cscale(Bs, wa), eq);
+      } else if (pass == 2) {
+        put_x(xm, xl, 0, r, jh, ir_scale(An, -rwa), ir_scale(As, -rwa), eq);
+        put_x(xm, xl, 4, r, jh, cscale(Bn, wa), cscale(Bs, wa), eq);
+      } else if (pass == 4) {
+        put_x(xm, xl, 0, r, jh, cscale(An, w), cscale(As, w), eq);
+        put_x(xm, xl, 1, r, jh, cscale(Bn, w), cscale(Bs, w), eq);
+      } else {
+        put_x(xm, xl, 3, r, jh, cscale(An, w), cscale(As, w), eq);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 int pick_threads(int work, bool bigp) {
   if (bigp) return work >= 128 ? 128 : 64;
   if (work >= 256) return 256;
@@ -436,7 +520,37 @@ int swe_launch(const PlanDev& P, const double2* eo, long long eo_mstride, double
   return kOk;
 }
 
+template <bool NONLIN, bool BIGP>
+int swe_prod_launch(const PlanDev& P, const double* grids, long long gfield, long long gmember,
+                    double* x, const XLayout& xl, int nmembers, double omega, double radius,
+                    cudaStream_t st) {
+  const size_t smem = sizeof(double2) * 2 * P.ring_stride;
+  SW_TRY(set_smem((const void*)swe_prod_kernel<NONLIN, BIGP>, smem));
+  dim3 gridDim(P.Jh, nmembers);
+  StageScope sc("swe_products", st);
+  swe_prod_kernel<NONLIN, BIGP><<<gridDim, BIGP ? 128 : 256, smem, st>>>(
+      P, grids, gfield, gmember, x, xl, omega, radius);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
 }  // namespace
+
+bool swe_grid_fits(const PlanDev& P) {
+  return sizeof(double2) * 7 * (size_t)P.ring_stride <= 160 * 1024;
+}
+
+int launch_swe_products(const PlanDev& P, bool nonlinear, const double* grids, long long gfield,
+                        long long gmember, double* x, const XLayout& xl, int nmembers,
+                        double omega, double radius, cudaStream_t st) {
+  const bool big = swfft::fft_needs_bigp(P.I);
+  if (nonlinear) {
+    if (big) return swe_prod_launch<true, true>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, st);
+    return swe_prod_launch<true, false>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, st);
+  }
+  if (big) return swe_prod_launch<false, true>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, st);
+  return swe_prod_launch<false, false>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, st);
+}
 
 int launch_fourier_to_grid(const PlanDev& P, const double2* eo, long long eo_fstride, double* grid,
                            long long grid_fstride, int nf, cudaStream_t st) {

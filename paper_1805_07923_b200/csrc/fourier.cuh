@@ -17,4 +17,12 @@ int launch_swe_grid(const PlanDev& P, bool nonlinear, const double2* eo, long lo
                     double* x, const XLayout& xl, int nmembers, double omega, double radius,
                     cudaStream_t st);
 
+// true when the fused grid kernel's 7 rings fit in shared memory
+bool swe_grid_fits(const PlanDev& P);
+// large-n_lon path: products + forward FFTs from 5 grids in HBM
+// (grids[m * gmember + q * gfield + il * J + j], q = U/a, V/a, zeta, delta, phi')
+int launch_swe_products(const PlanDev& P, bool nonlinear, const double* grids, long long gfield,
+                        long long gmember, double* x, const XLayout& xl, int nmembers,
+                        double omega, double radius, cudaStream_t st);
+
 }  // namespace swsdc
