@@ -71,6 +71,23 @@ int swsdc_analyze_divcurl(swsdc_plan* plan, const double* u, const double* v, in
 /* ShallowWaterRHS.eval_f_e (swe.py:251-279) for `batch` states. */
 int swsdc_eval_fe(swsdc_plan* plan, const swsdc_params* params, int include_nonlinear,
                   const double* state, int batch, double* out, void* stream);
+/* m-sharding (multi-GPU).  swsdc_set_row_filter(P, rank) makes every
+ * spectral-space kernel (solve, F_I, combine, resize, sweep node, analysis, F_E assembly)
+ * process only rows r with r % P == rank ((1, 0) = all rows).  The F_E pipeline is then
+ * run in stages with caller-owned exchange buffers so the caller can all-to-all between
+ * them: eo = [batch][5][R+1][ceil(J/2)][E.re,E.im,O.re,O.im] (rows of this rank),
+ * x = fragment-native analysis input (layout: swsdc_fe_layout) for latitude pairs
+ * [jh_begin, jh_end) and all rows. */
+int swsdc_set_row_filter(int mod, int rank);
+int swsdc_fe_layout(swsdc_plan* plan, int include_nonlinear, int batch, long long* eo_doubles,
+                    long long* x_doubles, int* x_nc, int* x_jh4);
+int swsdc_fe_synthesis(swsdc_plan* plan, const swsdc_params* params, const double* state, int batch,
+                       double* eo, void* stream);
+int swsdc_fe_grid(swsdc_plan* plan, const swsdc_params* params, int include_nonlinear,
+                  const double* eo, int batch, int jh_begin, int jh_end, double* x, void* stream);
+int swsdc_fe_analysis(swsdc_plan* plan, const swsdc_params* params, int include_nonlinear,
+                      const double* x, int batch, double* out, void* stream);
+
 /* ShallowWaterRHS.eval_f_i / eval_l_g (swe.py:206-217, 246-249). */
 int swsdc_eval_fi(int truncation, const swsdc_params* params, const double* state, int batch,
                   double* out, void* stream);

@@ -44,6 +44,12 @@ _SIGNATURES = {
     "swsdc_analyze_divcurl": ([_P, _P, _P, _I, _P, _P, _P], _I),
     "swsdc_eval_fe": ([_P, ctypes.POINTER(Params), _I, _P, _I, _P, _P], _I),
     "swsdc_eval_fi": ([_I, ctypes.POINTER(Params), _P, _I, _P, _P], _I),
+    "swsdc_set_row_filter": ([_I, _I], _I),
+    "swsdc_fe_layout": ([_P, _I, _I, ctypes.POINTER(_LL), ctypes.POINTER(_LL), ctypes.POINTER(_I),
+                         ctypes.POINTER(_I)], _I),
+    "swsdc_fe_synthesis": ([_P, ctypes.POINTER(Params), _P, _I, _P, _P], _I),
+    "swsdc_fe_grid": ([_P, ctypes.POINTER(Params), _I, _P, _I, _I, _I, _P, _P], _I),
+    "swsdc_fe_analysis": ([_P, ctypes.POINTER(Params), _I, _P, _I, _P, _P], _I),
     "swsdc_solve_implicit": ([_I, ctypes.POINTER(Params), _D, _P, _I, _P, _P], _I),
     "swsdc_combine": ([_I, ctypes.POINTER(_P), ctypes.POINTER(_D), _LL, _P, _P], _I),
     "swsdc_resize": ([_P, _I, _P, _I, _LL, _P], _I),

@@ -34,7 +34,23 @@ struct swsdc_plan {
   void* grid_ws = nullptr;      // large-n_lon F_E path: 5 grids per state
   size_t grid_bytes = 0;
   bool force_split = false;     // option 1: use the large-n_lon F_E path even when it fits
+  // m-sharding caches per row filter: balanced row pairs for synthesis and
+  // filtered analysis work lists
+  struct Shard {
+    int mod = 1, rank = 0;
+    int2* pairs = nullptr;
+    int npairs = 0;
+    int2* work[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    int nwork[2][2] = {{0, 0}, {0, 0}};
+    int nchunks[2] = {0, 0};
+  };
+  std::vector<Shard> shards;
+  std::vector<std::vector<int2>> host_work[2];  // host copies of the analysis lists
 };
+
+namespace swsdc {
+void set_row_filter(int mod, int rank);
+}
 
 namespace {
 
@@ -147,14 +163,57 @@ int syn_plain(swsdc_plan* p, const double2* coeffs, int r_in, int batch, double2
   return kOk;
 }
 
+// Pairs / work lists for the current row filter (nullptr = all rows).
+const swsdc_plan::Shard* shard_for(swsdc_plan* p) {
+  const RowFilter rf = current_row_filter();
+  if (rf.mod <= 1) return nullptr;
+  for (auto& s : p->shards)
+    if (s.mod == rf.mod && s.rank == rf.rank) return &s;
+  swsdc_plan::Shard s;
+  s.mod = rf.mod;
+  s.rank = rf.rank;
+  const int R = p->dev.R;
+  std::vector<int> rows;
+  for (int r = 0; r <= R; ++r)
+    if (r % rf.mod == rf.rank) rows.push_back(r);
+  std::vector<int2> pairs;
+  const int n = (int)rows.size();
+  for (int i = 0; i < (n + 1) / 2; ++i)
+    pairs.push_back(make_int2(rows[i], (n - 1 - i > i) ? rows[n - 1 - i] : -1));
+  s.npairs = (int)pairs.size();
+  if (!pairs.empty()) {
+    if (cudaMalloc(&s.pairs, sizeof(int2) * pairs.size()) != cudaSuccess) return nullptr;
+    cudaMemcpy(s.pairs, pairs.data(), sizeof(int2) * pairs.size(), cudaMemcpyHostToDevice);
+    p->owned.push_back(s.pairs);
+  }
+  for (int i = 0; i < 2; ++i) {
+    for (int r : rows) s.nchunks[i] += (R + i - r + 1 + kChunk - 1) / kChunk;
+    for (int j = 0; j < 2; ++j) {
+      std::vector<int2> w;
+      for (const int2& it : p->host_work[i][j])
+        if (it.x % rf.mod == rf.rank) w.push_back(it);
+      s.nwork[i][j] = (int)w.size();
+      if (!w.empty()) {
+        if (cudaMalloc(&s.work[i][j], sizeof(int2) * w.size()) != cudaSuccess) return nullptr;
+        cudaMemcpy(s.work[i][j], w.data(), sizeof(int2) * w.size(), cudaMemcpyHostToDevice);
+        p->owned.push_back(s.work[i][j]);
+      }
+    }
+  }
+  p->shards.push_back(s);
+  return &p->shards.back();
+}
+
 // Legendre analysis of the nv vectors (XLayout xl) of each member into out.
 int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, double2* out,
             long long out_vstride, long long out_rstride, long long out_mstride, int smax,
             bool zero_fill, cudaStream_t st) {
   const PlanDev& P = p->dev;
   const int which = (smax == P.R) ? 0 : 1;
+  const swsdc_plan::Shard* sh = shard_for(p);
+  const int nch = sh ? sh->nchunks[which] : p->nchunks[which];
   // split latitudes over 2 warps when the chunk tasks alone cannot fill the GPU
-  const int ls = ((long long)p->nchunks[which] * nmembers < 1800) ? 1 : 0;
+  const int ls = ((long long)nch * nmembers < 1800) ? 1 : 0;
   for (int v0 = 0; v0 < xl.nv; v0 += 16) {
     AnaArgs a{};
     a.nv = (xl.nv - v0 < 16) ? xl.nv - v0 : 16;
@@ -165,10 +224,12 @@ int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, dou
     a.out_rstride = out_rstride;
     a.smax = smax;
     a.zero_fill = zero_fill ? 1 : 0;
-    a.work = p->work[which][ls];
+    a.work = sh ? sh->work[which][ls] : p->work[which][ls];
     a.out_mstride = out_mstride;
     a.nmembers = nmembers;
-    SW_TRY(launch_analysis(P, a, p->nwork[which][ls], ls ? 2 : 1, st));
+    const int nw = sh ? sh->nwork[which][ls] : p->nwork[which][ls];
+    if (nw == 0) continue;
+    SW_TRY(launch_analysis(P, a, nw, ls ? 2 : 1, st));
   }
   return kOk;
 }
@@ -288,8 +349,13 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
     swsdc_plan_destroy(p);
     return st;
   }
-  for (int i = 0; i < 2; ++i)
-    for (int j = 0; j < 2; ++j) p->nwork[i][j] = (int)work[i][j].size();
+  for (int i = 0; i < 2; ++i) {
+    p->host_work[i].resize(2);
+    for (int j = 0; j < 2; ++j) {
+      p->nwork[i][j] = (int)work[i][j].size();
+      p->host_work[i][j] = work[i][j];
+    }
+  }
   void* ck = nullptr;
   if (cudaMalloc(&ck, sizeof(double2) * (size_t)nck * P.Jh) != cudaSuccess) {
     set_error("cudaMalloc of the checkpoint table failed");
@@ -437,6 +503,10 @@ int swsdc_eval_fe(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, c
   SW_TRY(check_params(q));
   if (batch < 0) { set_error("bad batch"); return kUsage; }
   if (batch == 0) return kOk;
+  if (current_row_filter().mod > 1) {
+    set_error("eval_fe under an m-sharding row filter: use the staged swsdc_fe_* calls");
+    return kUsage;
+  }
   const bool nl = include_nonlinear != 0;
   const int nv = nl ? 7 : 2;
   const size_t xb = x_bytes_for(p, nv, batch);
@@ -486,6 +556,100 @@ int swsdc_eval_fe(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, c
   SW_TRY(ana_run(p, x, xl, batch, y, yv, p->ldy, nv * yv, P.R + 1, false, S(stream)));
   return launch_finalize_swe(P, y, nv * yv, p->ldy, reinterpret_cast<double2*>(out), 3 * plane, nl,
                              q->radius, batch, S(stream));
+}
+
+int swsdc_set_row_filter(int mod, int rank) {
+  if (mod < 1 || rank < 0 || rank >= mod) { set_error("bad row filter"); return kUsage; }
+  set_row_filter(mod, rank);
+  return kOk;
+}
+
+int swsdc_fe_layout(swsdc_plan* p, int nonlinear, int batch, long long* eo_doubles,
+                    long long* x_doubles, int* x_nc, int* x_jh4) {
+  if (!p || batch < 0) { set_error("bad arguments"); return kUsage; }
+  const PlanDev& P = p->dev;
+  const XLayout xl = make_xlayout(P.R, P.Jh, nonlinear ? 7 : 2);
+  if (eo_doubles) *eo_doubles = (long long)batch * 5 * (P.R + 1) * P.Jh * 4;
+  if (x_doubles) *x_doubles = (long long)batch * xl.mstride;
+  if (x_nc) *x_nc = xl.nc;
+  if (x_jh4) *x_jh4 = xl.jh4;
+  return kOk;
+}
+
+int swsdc_fe_synthesis(swsdc_plan* p, const swsdc_params* q, const double* state, int batch,
+                       double* eo, void* stream) {
+  if (!p) { set_error("plan is NULL"); return kUsage; }
+  SW_TRY(check_params(q));
+  if (batch <= 0) return batch == 0 ? kOk : kUsage;
+  const PlanDev& P = p->dev;
+  const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
+  const long long plane = (long long)(P.R + 1) * (P.R + 1);
+  const swsdc_plan::Shard* sh = shard_for(p);
+  SynArgs a{};
+  a.src = reinterpret_cast<const double2*>(state);
+  a.src_fstride = plane;
+  a.src_R = P.R;
+  a.smax = P.R + 1;
+  a.radius = q->radius;
+  a.eo = reinterpret_cast<double2*>(eo);
+  a.src_mstride = 3 * plane;
+  a.eo_mstride = 5 * fstride;
+  a.nmembers = batch;
+  if (sh) {
+    a.pairs = sh->pairs;
+    a.npairs = sh->npairs;
+  }
+  return launch_synthesis(P, a, 5, kSynSWE, S(stream));
+}
+
+int swsdc_fe_grid(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, const double* eo,
+                  int batch, int jh_begin, int jh_end, double* x, void* stream) {
+  if (!p) { set_error("plan is NULL"); return kUsage; }
+  SW_TRY(check_params(q));
+  const PlanDev& P = p->dev;
+  if (jh_begin < 0 || jh_end > P.Jh || jh_begin > jh_end || batch < 0) {
+    set_error("bad latitude-pair range");
+    return kUsage;
+  }
+  if (batch == 0 || jh_begin == jh_end) return kOk;
+  const bool nl = include_nonlinear != 0;
+  const XLayout xl = make_xlayout(P.R, P.Jh, nl ? 7 : 2);
+  const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
+  const double2* e = reinterpret_cast<const double2*>(eo);
+  if (swe_grid_fits(P) && !p->force_split)
+    return launch_swe_grid(P, nl, e, 5 * fstride, x, xl, batch, q->omega, q->radius, S(stream),
+                           jh_begin, jh_end);
+  const long long gfield = (long long)P.I * P.J;
+  const size_t need = sizeof(double) * (size_t)gfield * 5 * batch;
+  if (need > p->grid_bytes) {
+    if (p->grid_ws) { SW_CUDA(cudaDeviceSynchronize()); SW_CUDA(cudaFree(p->grid_ws)); }
+    p->grid_ws = nullptr;
+    p->grid_bytes = 0;
+    SW_CUDA(cudaMalloc(&p->grid_ws, need));
+    p->grid_bytes = need;
+  }
+  double* g = reinterpret_cast<double*>(p->grid_ws);
+  SW_TRY(launch_fourier_to_grid(P, e, fstride, g, gfield, 5 * batch, S(stream), jh_begin, jh_end));
+  return launch_swe_products(P, nl, g, gfield, 5 * gfield, x, xl, batch, q->omega, q->radius,
+                             S(stream), jh_begin, jh_end);
+}
+
+int swsdc_fe_analysis(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, const double* x,
+                      int batch, double* out, void* stream) {
+  if (!p) { set_error("plan is NULL"); return kUsage; }
+  SW_TRY(check_params(q));
+  if (batch <= 0) return batch == 0 ? kOk : kUsage;
+  const PlanDev& P = p->dev;
+  const bool nl = include_nonlinear != 0;
+  const int nv = nl ? 7 : 2;
+  SW_TRY(ensure_ws(p, 0, 0, nv * batch, S(stream)));
+  const XLayout xl = make_xlayout(P.R, P.Jh, nv);
+  double2* y = ws_y(p, 0, 0);
+  const long long yv = (long long)(P.R + 1) * p->ldy;
+  const long long plane = (long long)(P.R + 1) * (P.R + 1);
+  SW_TRY(ana_run(p, x, xl, batch, y, yv, p->ldy, nv * yv, P.R + 1, false, S(stream)));
+  return launch_finalize_swe(P, y, nv * yv, p->ldy, reinterpret_cast<double2*>(out), 3 * plane, nl,
+                             q->radius, batch, S(stream), current_row_filter());
 }
 
 int swsdc_eval_fi(int R, const swsdc_params* q, const double* state, int batch, double* out,

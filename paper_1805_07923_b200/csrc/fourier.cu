@@ -168,19 +168,21 @@ __device__ __forceinline__ void put_x(double* x, const XLayout& L, int v, int r,
 // ---------------------------------------------------------------------------
 template <bool BIGP>
 __global__ void __launch_bounds__(256, 2) f2g_kernel(PlanDev P, const double2* eo, long long eo_fstride, double* grid,
-                           long long grid_fstride, int lnp) {
+                           long long grid_fstride, int lnp, int jh_begin, int jh_end) {
   extern __shared__ __align__(16) double2 rings[];
   const int np = 1 << lnp;
   const int f = blockIdx.y;
-  const int jh0 = blockIdx.x * np;
-  fill_rings(rings, P, eo + (size_t)f * eo_fstride, 0, 1, np, lnp, jh0);
+  const int jh0 = jh_begin + blockIdx.x * np;
+  PlanDev Q = P;
+  Q.Jh = jh_end;  // pairs >= jh_end are not this launch's (fill_rings bounds on Q.Jh)
+  fill_rings(rings, Q, eo + (size_t)f * eo_fstride, 0, 1, np, lnp, jh0);
   __syncthreads();
   fft_inverse<BIGP>(rings, np, P);
   double* g = grid + (size_t)f * grid_fstride;
   for (int idx = threadIdx.x; idx < (P.I << lnp); idx += blockDim.x) {
     const int il = idx >> lnp, i = idx & (np - 1);
     const int jh = jh0 + i;
-    if (jh >= P.Jh) continue;
+    if (jh >= jh_end) continue;
     const double2 z = rings[(size_t)i * P.ring_stride + swfft::pad_idx(il)];
     const int jn = jn_of(P, jh), js = js_of(P, jh);
     g[(size_t)il * P.J + jn] = z.x;
@@ -271,11 +273,11 @@ __global__ void __launch_bounds__(256, 2) g2f_kernel(PlanDev P, const double* gr
 // ---------------------------------------------------------------------------
 template <bool NONLIN, bool BIGP>
 __global__ void __launch_bounds__(256, 2) swe_grid_kernel(PlanDev P, const double2* eo, long long eo_mstride, double* x,
-                                XLayout xl, double omega, double radius) {
+                                XLayout xl, double omega, double radius, int jh_begin) {
   constexpr int NIN = NONLIN ? 5 : 4;
   constexpr int NPROD = NONLIN ? 7 : 2;
   extern __shared__ __align__(16) double2 rings[];  // [7 or 4][RS]
-  const int jh = blockIdx.x;
+  const int jh = jh_begin + blockIdx.x;
   const int m = blockIdx.y;
   const int RS = P.ring_stride;
   const size_t fstride = (size_t)(P.R + 1) * P.Jh * 2;
@@ -366,9 +368,9 @@ template <bool NONLIN, bool BIGP>
 __global__ void __launch_bounds__(256, 1) swe_prod_kernel(PlanDev P, const double* grids,
                                                           long long gfield, long long gmember,
                                                           double* x, XLayout xl, double omega,
-                                                          double radius) {
+                                                          double radius, int jh_begin) {
   extern __shared__ __align__(16) double2 rings[];  // [2][RS]
-  const int jh = blockIdx.x, m = blockIdx.y;
+  const int jh = jh_begin + blockIdx.x, m = blockIdx.y;
   const int RS = P.ring_stride, I = P.I;
   const int jn = jn_of(P, jh), js = js_of(P, jh);
   const bool eq = (jn == js);
@@ -473,14 +475,15 @@ int pairs_log2(const PlanDev& P, int nin) {
 
 template <bool BIGP>
 int f2g_launch(const PlanDev& P, const double2* eo, long long eo_fstride, double* grid,
-               long long grid_fstride, int nf, cudaStream_t st) {
+               long long grid_fstride, int nf, int jh_begin, int jh_end, cudaStream_t st) {
   const int lnp = pairs_log2(P, 1), np = 1 << lnp;
   const size_t smem = sizeof(double2) * np * P.ring_stride;
   SW_TRY(set_smem((const void*)f2g_kernel<BIGP>, smem));
-  dim3 gridDim((P.Jh + np - 1) / np, nf);
+  dim3 gridDim((jh_end - jh_begin + np - 1) / np, nf);
+  if (gridDim.x == 0) return kOk;
   StageScope sc("fourier_to_grid", st);
   f2g_kernel<BIGP><<<gridDim, pick_threads(np * max_butterflies(P), BIGP), smem, st>>>(
-      P, eo, eo_fstride, grid, grid_fstride, lnp);
+      P, eo, eo_fstride, grid, grid_fstride, lnp, jh_begin, jh_end);
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -502,10 +505,12 @@ int g2f_launch(const PlanDev& P, const double* grid, const double* grid2, long l
 
 template <bool NONLIN, bool BIGP>
 int swe_launch(const PlanDev& P, const double2* eo, long long eo_mstride, double* x,
-               const XLayout& xl, int nmembers, double omega, double radius, cudaStream_t st) {
+               const XLayout& xl, int nmembers, double omega, double radius, int jh_begin,
+               int jh_end, cudaStream_t st) {
   const int nr = NONLIN ? 7 : 4;
   const size_t smem = sizeof(double2) * nr * P.ring_stride;
-  dim3 gridDim(P.Jh, nmembers);
+  dim3 gridDim(jh_end - jh_begin, nmembers);
+  if (gridDim.x == 0) return kOk;
   SW_TRY(set_smem((const void*)swe_grid_kernel<NONLIN, BIGP>, smem));
   int threads = pick_threads(nr * max_butterflies(P), BIGP);
   while (threads * kSweMaxPts < P.I && threads < 256) threads *= 2;
@@ -515,7 +520,7 @@ int swe_launch(const PlanDev& P, const double2* eo, long long eo_mstride, double
   }
   StageScope sc("swe_grid", st);
   swe_grid_kernel<NONLIN, BIGP><<<gridDim, threads, smem, st>>>(
-      P, eo, eo_mstride, x, xl, omega, radius);
+      P, eo, eo_mstride, x, xl, omega, radius, jh_begin);
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -523,13 +528,14 @@ int swe_launch(const PlanDev& P, const double2* eo, long long eo_mstride, double
 template <bool NONLIN, bool BIGP>
 int swe_prod_launch(const PlanDev& P, const double* grids, long long gfield, long long gmember,
                     double* x, const XLayout& xl, int nmembers, double omega, double radius,
-                    cudaStream_t st) {
+                    int jh_begin, int jh_end, cudaStream_t st) {
   const size_t smem = sizeof(double2) * 2 * P.ring_stride;
   SW_TRY(set_smem((const void*)swe_prod_kernel<NONLIN, BIGP>, smem));
-  dim3 gridDim(P.Jh, nmembers);
+  dim3 gridDim(jh_end - jh_begin, nmembers);
+  if (gridDim.x == 0) return kOk;
   StageScope sc("swe_products", st);
   swe_prod_kernel<NONLIN, BIGP><<<gridDim, BIGP ? 128 : 256, smem, st>>>(
-      P, grids, gfield, gmember, x, xl, omega, radius);
+      P, grids, gfield, gmember, x, xl, omega, radius, jh_begin);
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -542,20 +548,24 @@ bool swe_grid_fits(const PlanDev& P) {
 
 int launch_swe_products(const PlanDev& P, bool nonlinear, const double* grids, long long gfield,
                         long long gmember, double* x, const XLayout& xl, int nmembers,
-                        double omega, double radius, cudaStream_t st) {
+                        double omega, double radius, cudaStream_t st, int jh_begin, int jh_end) {
+  if (jh_end < 0) jh_end = P.Jh;
   const bool big = swfft::fft_needs_bigp(P.I);
   if (nonlinear) {
-    if (big) return swe_prod_launch<true, true>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, st);
-    return swe_prod_launch<true, false>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, st);
+    if (big) return swe_prod_launch<true, true>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
+    return swe_prod_launch<true, false>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
   }
-  if (big) return swe_prod_launch<false, true>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, st);
-  return swe_prod_launch<false, false>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, st);
+  if (big) return swe_prod_launch<false, true>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
+  return swe_prod_launch<false, false>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
 }
 
 int launch_fourier_to_grid(const PlanDev& P, const double2* eo, long long eo_fstride, double* grid,
-                           long long grid_fstride, int nf, cudaStream_t st) {
-  if (swfft::fft_needs_bigp(P.I)) return f2g_launch<true>(P, eo, eo_fstride, grid, grid_fstride, nf, st);
-  return f2g_launch<false>(P, eo, eo_fstride, grid, grid_fstride, nf, st);
+                           long long grid_fstride, int nf, cudaStream_t st, int jh_begin,
+                           int jh_end) {
+  if (jh_end < 0) jh_end = P.Jh;
+  if (swfft::fft_needs_bigp(P.I))
+    return f2g_launch<true>(P, eo, eo_fstride, grid, grid_fstride, nf, jh_begin, jh_end, st);
+  return f2g_launch<false>(P, eo, eo_fstride, grid, grid_fstride, nf, jh_begin, jh_end, st);
 }
 
 int launch_grid_to_fourier(const PlanDev& P, int mode, const double* grid, const double* grid2,
@@ -572,14 +582,15 @@ int launch_grid_to_fourier(const PlanDev& P, int mode, const double* grid, const
 
 int launch_swe_grid(const PlanDev& P, bool nonlinear, const double2* eo, long long eo_mstride,
                     double* x, const XLayout& xl, int nmembers, double omega, double radius,
-                    cudaStream_t st) {
+                    cudaStream_t st, int jh_begin, int jh_end) {
+  if (jh_end < 0) jh_end = P.Jh;
   const bool big = swfft::fft_needs_bigp(P.I);
   if (nonlinear) {
-    if (big) return swe_launch<true, true>(P, eo, eo_mstride, x, xl, nmembers, omega, radius, st);
-    return swe_launch<true, false>(P, eo, eo_mstride, x, xl, nmembers, omega, radius, st);
+    if (big) return swe_launch<true, true>(P, eo, eo_mstride, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
+    return swe_launch<true, false>(P, eo, eo_mstride, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
   }
-  if (big) return swe_launch<false, true>(P, eo, eo_mstride, x, xl, nmembers, omega, radius, st);
-  return swe_launch<false, false>(P, eo, eo_mstride, x, xl, nmembers, omega, radius, st);
+  if (big) return swe_launch<false, true>(P, eo, eo_mstride, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
+  return swe_launch<false, false>(P, eo, eo_mstride, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
 }
 
 }  // namespace swsdc

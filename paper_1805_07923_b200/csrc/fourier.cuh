@@ -6,7 +6,8 @@ namespace swsdc {
 
 // (E, O) partial sums of nf fields -> grids [nf][I][J]
 int launch_fourier_to_grid(const PlanDev& P, const double2* eo, long long eo_fstride, double* grid,
-                           long long grid_fstride, int nf, cudaStream_t st);
+                           long long grid_fstride, int nf, cudaStream_t st, int jh_begin = 0,
+                           int jh_end = -1);
 // grids -> weighted (S, D) vectors in XLayout.  mode 0: plain (nf fields = nf
 // vectors of one member); mode 1: div/curl (nf (U, V) pairs = nf members of 4 vectors)
 int launch_grid_to_fourier(const PlanDev& P, int mode, const double* grid, const double* grid2,
@@ -15,7 +16,7 @@ int launch_grid_to_fourier(const PlanDev& P, int mode, const double* grid, const
 // fused eval_f_e grid stage for nmembers states
 int launch_swe_grid(const PlanDev& P, bool nonlinear, const double2* eo, long long eo_mstride,
                     double* x, const XLayout& xl, int nmembers, double omega, double radius,
-                    cudaStream_t st);
+                    cudaStream_t st, int jh_begin = 0, int jh_end = -1);
 
 // true when the fused grid kernel's 7 rings fit in shared memory
 bool swe_grid_fits(const PlanDev& P);
@@ -23,6 +24,7 @@ bool swe_grid_fits(const PlanDev& P);
 // (grids[m * gmember + q * gfield + il * J + j], q = U/a, V/a, zeta, delta, phi')
 int launch_swe_products(const PlanDev& P, bool nonlinear, const double* grids, long long gfield,
                         long long gmember, double* x, const XLayout& xl, int nmembers,
-                        double omega, double radius, cudaStream_t st);
+                        double omega, double radius, cudaStream_t st, int jh_begin = 0,
+                        int jh_end = -1);
 
 }  // namespace swsdc

@@ -234,7 +234,8 @@ syn_kernel(PlanDev P, SynArgs a) {
   a.eo += (size_t)blockIdx.z * a.eo_mstride;
 
   const int p = blockIdx.x, lg = blockIdx.y;
-  const int rows[2] = {p, P.R - p};
+  const int2 pr = a.pairs ? a.pairs[p] : make_int2(p, P.R - p);
+  const int rows[2] = {pr.x, pr.y};
   const bool two = rows[1] > rows[0];
   int nst[2], nch[2];
   for (int i = 0; i < 2; ++i) {
@@ -362,7 +363,8 @@ syn_kernel(PlanDev P, SynArgs a) {
 
 template <int B, int MODE, int NSPLIT>
 int launch_syn_t(const PlanDev& P, const SynArgs& a, cudaStream_t st) {
-  const int npairs = P.R / 2 + 1;
+  const int npairs = a.pairs ? a.npairs : P.R / 2 + 1;
+  if (npairs == 0) return kOk;
   const int nlg = (P.Jh + kSynLat - 1) / kSynLat;
   size_t smem = sizeof(double2) * NSPLIT * B * kCS + sizeof(double) * (NSPLIT * kCS + 2);
   if (NSPLIT > 1) smem += sizeof(double2) * NSPLIT * B * kSynLat * 2;
@@ -376,8 +378,8 @@ int launch_syn_t(const PlanDev& P, const SynArgs& a, cudaStream_t st) {
 }
 
 // Warps per CTA so the grid offers ~2 resident warps per SM sub-partition.
-int pick_split(const PlanDev& P, int nmembers) {
-  const long long base = (long long)(P.R / 2 + 1) * ((P.Jh + kSynLat - 1) / kSynLat) * nmembers;
+int pick_split(const PlanDev& P, int npairs, int nmembers) {
+  const long long base = (long long)npairs * ((P.Jh + kSynLat - 1) / kSynLat) * nmembers;
   if (base >= 1000) return 1;
   if (base >= 500) return 2;
   return 4;
@@ -385,7 +387,7 @@ int pick_split(const PlanDev& P, int nmembers) {
 
 template <int B, int MODE>
 int launch_syn_b(const PlanDev& P, const SynArgs& a, cudaStream_t st) {
-  switch (pick_split(P, a.nmembers)) {
+  switch (pick_split(P, a.pairs ? a.npairs : P.R / 2 + 1, a.nmembers)) {
     case 1: return launch_syn_t<B, MODE, 1>(P, a, st);
     case 2: return launch_syn_t<B, MODE, 2>(P, a, st);
     default: return launch_syn_t<B, MODE, 4>(P, a, st);

@@ -19,6 +19,8 @@ struct SynArgs {
   long long src_mstride;   // complex elements between members (blockIdx.y)
   long long eo_mstride;    // double2 elements between members
   int nmembers;            // independent states / field groups in one launch
+  const int2* pairs;       // optional row pairs (r1, r2; r2 < 0: single row); default {p, R-p}
+  int npairs;
   int nJB;                 // set by the launcher
 };
 

@@ -13,6 +13,11 @@
 #include "spectral.cuh"
 
 namespace swsdc {
+
+static thread_local RowFilter g_row_filter{1, 0};
+RowFilter current_row_filter() { return g_row_filter; }
+void set_row_filter(int mod, int rank) { g_row_filter = RowFilter{mod, rank}; }
+
 namespace {
 
 __device__ __forceinline__ double lam_of(int s, double radius) {
@@ -36,7 +41,7 @@ __device__ __forceinline__ double2 hshift(const double2* Yv, const double* eps_r
 
 __global__ void finalize_swe_kernel(PlanDev P, const double2* Y, long long y_mstride, int ldy,
                                     double2* out, long long out_mstride, int nonlin,
-                                    double radius, int nmembers) {
+                                    double radius, int nmembers, RowFilter rf) {
   const int R = P.R;
   const long long total = (long long)nmembers * (R + 1) * (R + 1);
   const long long plane = (long long)(R + 1) * (R + 1);
@@ -46,6 +51,7 @@ __global__ void finalize_swe_kernel(PlanDev P, const double2* Y, long long y_mst
     const int m = (int)(idx / plane);
     const int rs = (int)(idx - m * plane);
     const int r = rs / (R + 1), s = rs - r * (R + 1);
+    if (r % rf.mod != rf.rank) continue;
     double2* o = out + m * out_mstride + rs;
     double2 phi = make_double2(0.0, 0.0), zeta = phi, delta = phi;
     if (s >= r) {
@@ -100,7 +106,7 @@ __global__ void finalize_divcurl_kernel(PlanDev P, const double2* Y, long long y
 
 // state layout: [m][3][R+1][R+1] complex, fields (phi', zeta, delta)
 __global__ void eval_fi_kernel(int R, ModelConsts c, const double2* x, double2* out,
-                               long long nmat) {
+                               long long nmat, RowFilter rf) {
   const long long plane = (long long)(R + 1) * (R + 1);
   const long long total = nmat * plane;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -108,6 +114,7 @@ __global__ void eval_fi_kernel(int R, ModelConsts c, const double2* x, double2* 
     const long long m = idx / plane;
     const int rs = (int)(idx - m * plane);
     const int s = rs % (R + 1);
+    if ((rs / (R + 1)) % rf.mod != rf.rank) continue;
     const double lam = lam_of(s, c.radius);
     const double nl = c.nu * lam;
     const double2* xm = x + m * 3 * plane + rs;
@@ -120,7 +127,7 @@ __global__ void eval_fi_kernel(int R, ModelConsts c, const double2* x, double2* 
 }
 
 __global__ void solve_kernel(int R, ModelConsts c, double beta, const double2* b, double2* out,
-                             long long nmat) {
+                             long long nmat, RowFilter rf) {
   const long long plane = (long long)(R + 1) * (R + 1);
   const long long total = nmat * plane;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -128,6 +135,7 @@ __global__ void solve_kernel(int R, ModelConsts c, double beta, const double2* b
     const long long m = idx / plane;
     const int rs = (int)(idx - m * plane);
     const int s = rs % (R + 1);
+    if ((rs / (R + 1)) % rf.mod != rf.rank) continue;
     const double lam = lam_of(s, c.radius);
     const double d = 1.0 - beta * c.nu * lam;
     const double det = d * d - beta * beta * lam * c.phi_bar;
@@ -152,7 +160,8 @@ __global__ void combine_kernel(CombineArgs a, long long count) {
   }
 }
 
-__global__ void resize_kernel(const double2* in, int rin, double2* out, int rout, long long nmat) {
+__global__ void resize_kernel(const double2* in, int rin, double2* out, int rout, long long nmat,
+                              RowFilter rf) {
   const long long plane = (long long)(rout + 1) * (rout + 1);
   const long long total = nmat * plane;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -160,13 +169,14 @@ __global__ void resize_kernel(const double2* in, int rin, double2* out, int rout
     const long long m = idx / plane;
     const int rs = (int)(idx - m * plane);
     const int r = rs / (rout + 1), s = rs - r * (rout + 1);
+    if (r % rf.mod != rf.rank) continue;
     double2 v = make_double2(0.0, 0.0);
     if (r <= rin && s <= rin) v = in[m * (long long)(rin + 1) * (rin + 1) + (long long)r * (rin + 1) + s];
     out[idx] = v;
   }
 }
 
-__global__ void spec_combine_kernel(SpecCombineArgs a, long long nmat) {
+__global__ void spec_combine_kernel(SpecCombineArgs a, long long nmat, RowFilter rf) {
   const int ro = a.rout;
   const long long plane = (long long)(ro + 1) * (ro + 1);
   const long long total = nmat * plane;
@@ -175,6 +185,7 @@ __global__ void spec_combine_kernel(SpecCombineArgs a, long long nmat) {
     const long long m = idx / plane;
     const int rs = (int)(idx - m * plane);
     const int r = rs / (ro + 1), s = rs - r * (ro + 1);
+    if (r % rf.mod != rf.rank) continue;
     double2 acc = make_double2(0.0, 0.0);
     for (int k = 0; k < a.n; ++k) {
       const int ri = a.rin[k];
@@ -190,7 +201,7 @@ __global__ void spec_combine_kernel(SpecCombineArgs a, long long nmat) {
 
 // b = sum_k w_k x_k -> theta = (I - beta F_I)^-1 b -> fi = L_G(theta)
 __global__ void sweep_node_kernel(int R, ModelConsts c, double beta, SpecCombineArgs a,
-                                  double2* theta, double2* fi, long long nstates) {
+                                  double2* theta, double2* fi, long long nstates, RowFilter rf) {
   const long long plane = (long long)(R + 1) * (R + 1);
   const long long total = nstates * plane;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -198,6 +209,7 @@ __global__ void sweep_node_kernel(int R, ModelConsts c, double beta, SpecCombine
     const long long m = idx / plane;
     const int rs = (int)(idx - m * plane);
     const int s = rs % (R + 1);
+    if ((rs / (R + 1)) % rf.mod != rf.rank) continue;
     const long long o = m * 3 * plane + rs;
     double2 b[3];
 #pragma unroll
@@ -239,11 +251,11 @@ int grid_for(long long n, int threads) {
 
 int launch_finalize_swe(const PlanDev& P, const double2* Y, long long y_mstride, int ldy,
                         double2* out, long long out_mstride, bool nonlin, double radius,
-                        int nmembers, cudaStream_t st) {
+                        int nmembers, cudaStream_t st, RowFilter rf) {
   const long long n = (long long)nmembers * (P.R + 1) * (P.R + 1);
   StageScope sc("finalize_swe", st);
   finalize_swe_kernel<<<grid_for(n, 256), 256, 0, st>>>(P, Y, y_mstride, ldy, out, out_mstride,
-                                                        nonlin ? 1 : 0, radius, nmembers);
+                                                        nonlin ? 1 : 0, radius, nmembers, rf);
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -262,7 +274,7 @@ int launch_eval_fi(int R, const ModelConsts& c, const double2* x, double2* out, 
                    cudaStream_t st) {
   const long long n = nmat * (R + 1) * (R + 1);
   StageScope sc("eval_fi", st);
-  eval_fi_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, x, out, nmat);
+  eval_fi_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, x, out, nmat, current_row_filter());
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -271,7 +283,7 @@ int launch_solve(int R, const ModelConsts& c, double beta, const double2* b, dou
                  long long nmat, cudaStream_t st) {
   const long long n = nmat * (R + 1) * (R + 1);
   StageScope sc("solve_implicit", st);
-  solve_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, beta, b, out, nmat);
+  solve_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, beta, b, out, nmat, current_row_filter());
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -286,7 +298,7 @@ int launch_combine(const CombineArgs& a, long long count, cudaStream_t st) {
 int launch_spec_combine(const SpecCombineArgs& a, long long nmat, cudaStream_t st) {
   const long long n = nmat * (a.rout + 1) * (a.rout + 1);
   StageScope sc("spec_combine", st);
-  spec_combine_kernel<<<grid_for(n, 256), 256, 0, st>>>(a, nmat);
+  spec_combine_kernel<<<grid_for(n, 256), 256, 0, st>>>(a, nmat, current_row_filter());
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -295,7 +307,8 @@ int launch_sweep_node(int R, const ModelConsts& c, double beta, const SpecCombin
                       double2* theta, double2* fi, long long nstates, cudaStream_t st) {
   const long long n = nstates * (R + 1) * (R + 1);
   StageScope sc("sweep_node", st);
-  sweep_node_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, beta, a, theta, fi, nstates);
+  sweep_node_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, beta, a, theta, fi, nstates,
+                                                       current_row_filter());
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -304,7 +317,7 @@ int launch_resize(const double2* in, int rin, double2* out, int rout, long long 
                   cudaStream_t st) {
   const long long n = nmat * (rout + 1) * (rout + 1);
   StageScope sc("resize", st);
-  resize_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, rin, out, rout, nmat);
+  resize_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, rin, out, rout, nmat, current_row_filter());
   SW_LAUNCH_CHECK();
   return kOk;
 }

@@ -8,6 +8,13 @@ struct ModelConsts {
   double radius, omega, gravity, nu, h_bar, phi_bar;
 };
 
+// Rows r with r % mod == rank are processed (m-sharding, cyclic in r); other
+// rows are neither read nor written.  {1, 0} = all rows.
+struct RowFilter {
+  int mod, rank;
+};
+RowFilter current_row_filter();
+
 constexpr int kMaxCombine = 32;
 struct CombineArgs {
   const double* x[kMaxCombine];
@@ -18,7 +25,7 @@ struct CombineArgs {
 
 int launch_finalize_swe(const PlanDev& P, const double2* Y, long long y_mstride, int ldy,
                         double2* out, long long out_mstride, bool nonlin, double radius,
-                        int nmembers, cudaStream_t st);
+                        int nmembers, cudaStream_t st, RowFilter rf = {1, 0});
 int launch_finalize_divcurl(const PlanDev& P, const double2* Y, long long y_mstride, int ldy,
                             double2* div, double2* curl, int nmembers, cudaStream_t st);
 int launch_eval_fi(int R, const ModelConsts& c, const double2* x, double2* out, long long nmat,
