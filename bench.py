@@ -320,7 +320,7 @@ def run_ours(args, world, rank, local):
     mlsdc_lines = {}
     if not args.no_mlsdc:
         for name, cfg in MLSDC_CONFIGS.items():
-            if world > 1 and cfg[10] == 1:
+            if world > 1 and cfg[10] == 1 and name not in SHARDED:
                 continue   # single-state configs run on one GPU only
             mlsdc_lines[name] = run_mlsdc(name, cfg, world, rank, dev, dist, flush_l2, peak_fp64)
 
@@ -415,7 +415,10 @@ MLSDC_CONFIGS = {
     "config0": (63, (192, 96), 31, (96, 48), 3, 2, 2, 1, 600.0, 1, 1),
     "config2": (255, (768, 384), 127, (384, 192), 5, 3, 4, 2, 240.0, 10, 1),
     "config4": (170, (512, 256), 85, (256, 128), 3, 2, 2, 1, 450.0, 1, 64),
+    # m-sharded across ranks when N > 1 (cyclic rows + latitude pairs, NCCL all-to-all)
+    "config3": (1279, (3840, 1920), 639, (1920, 960), 3, 2, 2, 1, 60.0, 1, 1),
 }
+SHARDED = {"config3"}
 
 
 def mlsdc_flops(cfg):
@@ -437,6 +440,8 @@ def run_mlsdc(name, cfg, world, rank, dev, dist, flush_l2, peak_fp64):
     mine = members // world if members >= world else members
     first = rank * mine if members >= world else 0
     params = swe.ModelParams(**workloads.EARTH)
+    if name in SHARDED and world > 1:
+        return run_sharded(name, cfg, world, rank, dev, dist, flush_l2, peak_fp64)
     hier = mlsdc.build_hierarchy(params, Rf, nf, Rc, nc, grid_fine=gf, grid_coarse=gc, device=dev)
     if members > 1:
         x0 = np.stack([workloads.seeded_state(Rf, k) for k in range(first, first + mine)])
@@ -479,6 +484,45 @@ def run_mlsdc(name, cfg, world, rank, dev, dist, flush_l2, peak_fp64):
     return out
 
 
+def run_sharded(name, cfg, world, rank, dev, dist, flush_l2, peak_fp64):
+    """One state m-sharded over all ranks (distributed.py); eager stepping (the
+    NCCL all-to-alls are not graph-captured)."""
+    import torch
+    from paper_1805_07923_b200 import distributed as D, swe, workloads
+    Rf, gf, Rc, gc, nf, nc, n_it, ncs, dt, steps, members = cfg
+    params = swe.ModelParams(**workloads.EARTH)
+    ex = D.TorchExchanger()
+    spec = D.ShardSpec(world, rank)
+    hier = D.sharded_hierarchy(params, Rf, nf, Rc, nc, ex, spec, grid_fine=gf, grid_coarse=gc,
+                               device=dev)
+    st0 = swe.PrognosticState(torch.as_tensor(workloads.seeded_state(Rf, 0), device=dev))
+    D.sharded_mlsdc_timestep(st0, dt, n_it, hier, spec, ncs)   # warm-up
+    torch.cuda.synchronize()
+    dist.barrier()
+    t_ms = 0.0
+    st = st0
+    for _ in range(steps):
+        flush_l2()
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        st = D.sharded_mlsdc_timestep(st, dt, n_it, hier, spec, ncs)
+        b_.record()
+        torch.cuda.synchronize()
+        t_ms += a.elapsed_time(b_)
+    t_ms = max_over_ranks(t_ms, dist, dev)
+    full = D.gather_state(ex, spec, st.data)
+    finite = bool(torch.isfinite(torch.view_as_real(full)).all())
+    fl = mlsdc_flops(cfg)
+    return {"metric": "MLSDC-SH fine sweeps/s (fp64)", "value": n_it * steps / (t_ms * 1e-3),
+            "unit": "fine sweeps/s", "ms_per_step": t_ms / steps, "steps": steps, "members": 1,
+            "config": {"R": [Rf, Rc], "grid": [list(gf), list(gc)], "nodes": [nf, nc],
+                       "iterations": n_it, "coarse_sweeps": ncs, "dt": dt,
+                       "parallelism": f"m-sharded x{world} (cyclic rows, latitude pairs, NCCL all-to-all)"},
+            "step_fp64_tflops": fl / (t_ms * 1e-3 / steps) / 1e12,
+            "step_frac_fp64_per_gpu": fl / (t_ms * 1e-3 / steps) / 1e12 / peak_fp64 / world,
+            "scaling": "strong", "finite": finite}
+
+
 def _cpu_mlsdc(args):
     """Oracle time for ONE step of an MLSDC config (1 core)."""
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
@@ -497,6 +541,9 @@ def _cpu_mlsdc(args):
 
 def cpu_mlsdc_baseline(name):
     import multiprocessing as mp
+    if name == "config3":
+        return {"value": None, "unit": "fine sweeps/s", "cores": 0, "kind": "port",
+                "sample": "N/A: the reference's dense (R+1,R+1,J) tables need 126 GB at T1279"}
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     cfg = MLSDC_CONFIGS[name]
     n_it, members = cfg[6], cfg[10]
