@@ -136,7 +136,9 @@ int syn_plain(swsdc_plan* p, const double2* coeffs, int r_in, int batch, double2
   const long long cin = (long long)(r_in + 1) * (r_in + 1);
   const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
   int B = 0;
-  for (int cand = 6; cand >= 4; --cand)
+  const char* fb = getenv("SWSDC_SYN_B");   // tuning knob: fields per synthesis CTA
+  if (fb && batch % atoi(fb) == 0) B = atoi(fb);
+  for (int cand = 6; cand >= 4 && !B; --cand)
     if (batch % cand == 0) { B = cand; break; }
   int done = 0;
   while (done < batch) {
