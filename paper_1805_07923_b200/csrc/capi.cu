@@ -215,7 +215,8 @@ int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, dou
   const swsdc_plan::Shard* sh = shard_for(p);
   const int nch = sh ? sh->nchunks[which] : p->nchunks[which];
   // split latitudes over 2 warps when the chunk tasks alone cannot fill the GPU
-  const int ls = ((long long)nch * nmembers < 1800) ? 1 : 0;
+  const int nv0 = xl.nv < 16 ? xl.nv : 16;
+  const int ls = (!ana_uses_tma(nv0) && (long long)nch * nmembers < 1800) ? 1 : 0;
   for (int v0 = 0; v0 < xl.nv; v0 += 16) {
     AnaArgs a{};
     a.nv = (xl.nv - v0 < 16) ? xl.nv - v0 : 16;

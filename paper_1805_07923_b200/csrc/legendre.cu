@@ -620,13 +620,220 @@ int launch_ana_nt(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, cud
   return launch_ana_t<NT, 1>(P, a, nwork, st);
 }
 
+// ---------------------------------------------------------------------------
+// Analysis, TMA-streamed variant (default).  CTA = 4 warps = 4 consecutive
+// 32-degree chunks of ONE row r; the row's x tiles (32 latitudes = 8 blocks,
+// contiguous in the fragment-native layout) are streamed into a 3-deep shared
+// ring by one elected thread with cp.async.bulk (TMA, SASS UBLKCP) completing
+// on an mbarrier, so the B fragments of every warp are conflict-free smem
+// loads instead of L2 round trips; each warp regenerates its own q tile and
+// runs the DMMA k-steps as before.
+// ---------------------------------------------------------------------------
+constexpr int kTmaBuf = 3;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                             unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kAnaWarps * 32)
+ana_tma_kernel(PlanDev P, AnaArgs a) {
+  extern __shared__ __align__(128) double smem[];
+  const int nc = a.xl.nc;                        // layout columns (>= 8 NT)
+  const int blk_doubles = 8 * 2 * nc * 4;        // one 32-latitude tile
+  double* xbuf = smem;                           // [kTmaBuf][blk_doubles]
+  double* wsm = xbuf + kTmaBuf * blk_doubles;    // per-warp q tile + betas
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(
+      wsm + kAnaWarps * (kChunk * kQS + kChunk));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double* qs = wsm + (size_t)warp * (kChunk * kQS + kChunk);
+  double* bs = qs + kChunk * kQS;
+
+  const double* x = a.x + (size_t)blockIdx.y * a.xl.mstride;
+  double2* out = a.out + (size_t)blockIdx.y * a.out_mstride;
+  const int2 wk = a.work[blockIdx.x];
+  const int r = wk.x, c = wk.y + warp;
+  const int nout = a.smax - r + 1;
+  const bool active = c * kChunk < nout;
+
+  if (a.zero_fill && wk.y == 0 && warp == 0) {
+    for (int idx = lane; idx < a.nv * r; idx += 32) {
+      const int v = idx / r, s = idx - v * r;
+      out[(size_t)v * a.out_vstride + (size_t)r * a.out_rstride + s] = make_double2(0.0, 0.0);
+    }
+  }
+  const int jh4 = a.xl.jh4;
+  const int nblk = (P.Jh + 31) >> 5;
+  const double* xr = x + (size_t)r * jh4 * 2 * nc * 4;
+  auto issue = [&](int jb32) {
+    const int nb = min(8, jh4 - 8 * jb32);
+    const unsigned bytes = (unsigned)(nb * 2 * nc * 4 * sizeof(double));
+    unsigned long long* bar = &bars[jb32 % kTmaBuf];
+    mbar_expect_tx(bar, bytes);
+    tma_bulk_g2s(xbuf + (size_t)(jb32 % kTmaBuf) * blk_doubles, xr + (size_t)jb32 * blk_doubles,
+                 bytes, bar);
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTmaBuf; ++i) mbar_init(&bars[i], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kTmaBuf - 1 && i < nblk; ++i) issue(i);
+
+  double acc[2][2][NT][2];
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int n = 0; n < NT; ++n) { acc[p][mt][n][0] = 0.0; acc[p][mt][n][1] = 0.0; }
+
+  const int k0 = c * kChunk;
+  const double2* seeds = P.ckpt + (size_t)(P.ck_off[r] + (active ? c : 0)) * P.Jh;
+  if (active) bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
+  const int ncol = 2 * a.nv;
+  double2 sd_nx = make_double2(0.0, 0.0);
+  double mu_nx = 0.0;
+  if (active && lane < P.Jh) { sd_nx = seeds[lane]; mu_nx = P.mu_n[lane]; }
+
+  for (int jb32 = 0; jb32 < nblk; ++jb32) {
+    // refill: the slot of block jb32-1 is free once every warp passed the barrier
+    __syncthreads();
+    if (threadIdx.x == 0 && jb32 + kTmaBuf - 1 < nblk) issue(jb32 + kTmaBuf - 1);
+    if (active) {
+      const int jh = (jb32 << 5) + lane;
+      const double2 sd = sd_nx;
+      const double mu = mu_nx;
+      {
+        const int jn = ((jb32 + 1) << 5) + lane;
+        if (jn < P.Jh) { sd_nx = seeds[jn]; mu_nx = P.mu_n[jn]; }
+      }
+      if (jh < P.Jh) {
+        double qa = sd.x, qb = sd.y;
+        qs[lane] = qa;
+        qs[16 * kQS + lane] = qb;
+#pragma unroll
+        for (int kk = 2; kk < kChunk; kk += 2) {
+          qa = fma(mu, qb, -bs[kk] * qa);
+          qb = fma(mu, qa, -bs[kk + 1] * qb);
+          qs[(kk >> 1) * kQS + lane] = qa;
+          qs[(16 + (kk >> 1)) * kQS + lane] = qb;
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < kChunk; ++kk) qs[((kk & 1) * 16 + (kk >> 1)) * kQS + lane] = 0.0;
+      }
+      __syncwarp();
+      mbar_wait(&bars[jb32 % kTmaBuf], (unsigned)((jb32 / kTmaBuf) & 1));
+      const double* xb = xbuf + (size_t)(jb32 % kTmaBuf) * blk_doubles;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const bool ok = ((jb32 << 5) + s * 4 + t) < P.Jh;
+        double bv[2][NT];
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+          for (int n = 0; n < NT; ++n)
+            bv[p][n] = (ok && (n * 8 + g) < ncol) ? xb[((s * 2 + p) * nc + n * 8) * 4 + lane] : 0.0;
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const double av = qs[(p * 16 + mt * 8 + g) * kQS + s * 4 + t];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) dmma884(acc[p][mt][n], av, bv[p][n]);
+          }
+      }
+      __syncwarp();
+    }
+  }
+  if (!active) return;
+  const double* gr = P.gsc + (size_t)r * P.ldk;
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int k = k0 + p + 2 * (8 * mt + g);
+      if (k >= nout) continue;
+      const double gs = gr[k];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const int v = n * 4 + t;
+        if (v < a.nv)
+          out[(size_t)v * a.out_vstride + (size_t)r * a.out_rstride + r + k] =
+              make_double2(acc[p][mt][n][0] * gs, acc[p][mt][n][1] * gs);
+      }
+    }
+}
+
+template <int NT>
+int launch_ana_tma(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st) {
+  const size_t smem = sizeof(double) * ((size_t)kTmaBuf * 8 * 2 * a.xl.nc * 4 +
+                                        kAnaWarps * (kChunk * kQS + kChunk)) +
+                      sizeof(unsigned long long) * kTmaBuf + 16;
+  auto kern = ana_tma_kernel<NT>;
+  SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  StageScope sc("legendre_analysis", st);
+  kern<<<dim3(nwork, a.nmembers), kAnaWarps * 32, smem, st>>>(P, a);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
 }  // namespace
 
 int ana_warps_per_cta() { return kAnaWarps; }
 
-// a.work must list CTAs of kAnaWarps / lsplit consecutive chunks.
+// TMA-streamed analysis for <= 8 vectors (x tiles <= 8 KB: 3-4 CTAs/SM); the
+// register-prefetch kernel for wider batches, whose 16 KB tiles would limit
+// occupancy to 2 CTAs/SM.
+bool ana_uses_tma(int nv) {
+  const char* e = getenv("SWSDC_ANA_TMA");   // tuning knob: 0 = never, 2 = always
+  if (e && atoi(e) == 0) return false;
+  if (e && atoi(e) == 2) return true;
+  return nv <= 8;
+}
+
+// a.work must list CTAs of kAnaWarps / lsplit consecutive chunks (lsplit 1 for TMA).
 int launch_analysis(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, cudaStream_t st) {
   if (a.nv <= 0) return kOk;
+  if (ana_uses_tma(a.nv) && lsplit == 1) {
+    if (a.nv <= 4) return launch_ana_tma<1>(P, a, nwork, st);
+    if (a.nv <= 8) return launch_ana_tma<2>(P, a, nwork, st);
+    if (a.nv <= 12) return launch_ana_tma<3>(P, a, nwork, st);
+    if (a.nv <= 16) return launch_ana_tma<4>(P, a, nwork, st);
+  }
   if (a.nv <= 4) return launch_ana_nt<1>(P, a, nwork, lsplit, st);
   if (a.nv <= 8) return launch_ana_nt<2>(P, a, nwork, lsplit, st);
   if (a.nv <= 12) return launch_ana_nt<3>(P, a, nwork, lsplit, st);

@@ -46,5 +46,6 @@ int build_checkpoints(const PlanDev& P, const double* a_tab, const double* b_tab
 int launch_synthesis(const PlanDev& P, const SynArgs& a, int B, int mode, cudaStream_t st);
 int launch_analysis(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, cudaStream_t st);
 int ana_warps_per_cta();
+bool ana_uses_tma(int nv);
 
 }  // namespace swsdc
