@@ -216,7 +216,8 @@ int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, dou
   const int nch = sh ? sh->nchunks[which] : p->nchunks[which];
   // split latitudes over 2 warps when the chunk tasks alone cannot fill the GPU
   const int nv0 = xl.nv < 16 ? xl.nv : 16;
-  const int ls = (!ana_uses_tma(nv0) && (long long)nch * nmembers < 1800) ? 1 : 0;
+  int ls = (!ana_uses_tma(nv0) && (long long)nch * nmembers < 1800) ? 1 : 0;
+  if (const char* e = getenv("SWSDC_ANA_LSPLIT")) ls = (atoi(e) == 2 && !ana_uses_tma(nv0)) ? 1 : 0;
   for (int v0 = 0; v0 < xl.nv; v0 += 16) {
     AnaArgs a{};
     a.nv = (xl.nv - v0 < 16) ? xl.nv - v0 : 16;
