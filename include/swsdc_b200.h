@@ -114,6 +114,23 @@ int swsdc_sweep_node(int truncation, const swsdc_params* params, double beta, in
 /* spharm.truncate / spharm.pad (spharm.py:331-349) over `nmat` (R+1)^2 matrices. */
 int swsdc_resize(const double* in, int r_in, double* out, int r_out, long long nmat, void* stream);
 
+/* Upload of `nmat` dense (R+1)^2 spectral matrices from page-locked host memory
+ * (cudaHostAlloc / cudaHostRegister) to device `out`: only the s >= r triangle the
+ * reference layout populates crosses PCIe (zero-copy reads); the device copy's lower
+ * triangle is written as zeros.  The host-input half of TransformPlan.synthesize
+ * (spharm.py:258-260) for host arrays; 1 when `host` is not page-locked. */
+int swsdc_upload_coeffs(const double* host, int truncation, long long nmat, double* out,
+                        void* stream);
+
+/* Download of `nmat` dense (R+1)^2 spectral matrices from device `dev` into page-locked
+ * host memory by zero-copy stores.  write_lower = 1 writes the full dense matrices (the
+ * reference's analyze result, spharm.py:254-256); write_lower = 0 guarantees only the s >= r
+ * triangle: each entry below it is either left untouched or receives the device's value
+ * (~half the PCIe bytes, for callers streaming results into a reused, zero-initialised
+ * buffer, where either way it holds the reference's zero). */
+int swsdc_download_coeffs(const double* dev, int truncation, long long nmat, double* host,
+                          int write_lower, void* stream);
+
 /* Launch accounting / stage timing (bench.py): number of kernels launched by
  * this library so far; per-stage CUDA-event timing on/off (clears records);
  * collect "stage<TAB>launches<TAB>total_ms" lines, returns bytes needed. */

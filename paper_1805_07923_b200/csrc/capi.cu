@@ -136,8 +136,8 @@ int syn_plain(swsdc_plan* p, const double2* coeffs, int r_in, int batch, double2
   const long long cin = (long long)(r_in + 1) * (r_in + 1);
   const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
   int B = 0;
-  const char* fb = getenv("SWSDC_SYN_B");   // tuning knob: fields per synthesis CTA
-  if (fb && batch % atoi(fb) == 0) B = atoi(fb);
+  static const int fb = env_int("SWSDC_SYN_B", 0);   // tuning knob: fields per synthesis CTA
+  if (fb > 0 && batch % fb == 0) B = fb;
   for (int cand = 6; cand >= 4 && !B; --cand)
     if (batch % cand == 0) { B = cand; break; }
   int done = 0;
@@ -217,7 +217,8 @@ int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, dou
   // split latitudes over 2 warps when the chunk tasks alone cannot fill the GPU
   const int nv0 = xl.nv < 16 ? xl.nv : 16;
   int ls = (!ana_uses_tma(nv0) && (long long)nch * nmembers < 1800) ? 1 : 0;
-  if (const char* e = getenv("SWSDC_ANA_LSPLIT")) ls = (atoi(e) == 2 && !ana_uses_tma(nv0)) ? 1 : 0;
+  static const int knob = env_int("SWSDC_ANA_LSPLIT", 0);   // tuning knob: 1 or 2
+  if (knob) ls = (knob == 2 && !ana_uses_tma(nv0)) ? 1 : 0;
   for (int v0 = 0; v0 < xl.nv; v0 += 16) {
     AnaArgs a{};
     a.nv = (xl.nv - v0 < 16) ? xl.nv - v0 : 16;
@@ -756,6 +757,87 @@ int swsdc_resize(const double* in, int r_in, double* out, int r_out, long long n
   if (nmat == 0) return kOk;
   return launch_resize(reinterpret_cast<const double2*>(in), r_in, reinterpret_cast<double2*>(out),
                        r_out, nmat, S(stream));
+}
+
+// Staircase cover of the s >= r triangle: block k holds rows [r0, r1) and
+// columns [r0, R]; one 3D copy (rows x columns x matrices) per block on the copy
+// engine.  kStair blocks send 1/2 + 1/(2 kStair) of the dense bytes.
+static int stair_blocks() {
+  static const int k = std::max(1, env_int("SWSDC_STAIR_BLOCKS", 4));
+  return k;
+}
+
+static int stair_copy(const double2* src, double2* dst, int R, long long nmat, cudaMemcpyKind kind,
+                      cudaStream_t st) {
+  const int n = R + 1, K = std::min(stair_blocks(), n);
+  const size_t pitch = sizeof(double2) * n;
+  for (int k = 0; k < K; ++k) {
+    const int r0 = (int)((long long)n * k / K), r1 = (int)((long long)n * (k + 1) / K);
+    if (r1 <= r0) continue;
+    cudaMemcpy3DParms m{};
+    m.srcPtr = make_cudaPitchedPtr(const_cast<double2*>(src), pitch, pitch, n);
+    m.dstPtr = make_cudaPitchedPtr(dst, pitch, pitch, n);
+    m.srcPos = make_cudaPos(sizeof(double2) * r0, r0, 0);
+    m.dstPos = m.srcPos;
+    m.extent = make_cudaExtent(sizeof(double2) * (n - r0), r1 - r0, nmat);
+    m.kind = kind;
+    SW_CUDA(cudaMemcpy3DAsync(&m, st));
+  }
+  return kOk;
+}
+
+// Transfer engines (tuning knobs): 0 = zero-copy kernel, 1 = copy-engine staircase.
+// Measured at config 1 (bench.py e2e): strided copy-engine transfers are slow
+// host->device (a 5-matrix staircase upload took 130-160 us vs 55 us zero-copy),
+// while SM-driven zero-copy traffic slows concurrent transforms; the best mix is
+// a zero-copy upload on 32 CTAs and a 4-block staircase download.
+static int upload_mode() {
+  static const int m = env_int("SWSDC_UPLOAD_MODE", 0);
+  return m;
+}
+static int download_mode() {
+  static const int m = env_int("SWSDC_DOWNLOAD_MODE", 1);
+  return m;
+}
+
+int swsdc_upload_coeffs(const double* host, int r, long long nmat, double* out, void* stream) {
+  if (r < 0 || nmat < 0) { set_error("bad upload arguments"); return kUsage; }
+  if (nmat == 0) return kOk;
+  void* dptr = nullptr;
+  if (cudaHostGetDevicePointer(&dptr, const_cast<double*>(host), 0) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("swsdc_upload_coeffs: source is not page-locked host memory");
+    return kUsage;
+  }
+  if (upload_mode() == 0)
+    return launch_upload_triangle(reinterpret_cast<const double2*>(dptr),
+                                  reinterpret_cast<double2*>(out), r, nmat, S(stream));
+  SW_TRY(stair_copy(reinterpret_cast<const double2*>(host), reinterpret_cast<double2*>(out), r, nmat,
+                    cudaMemcpyHostToDevice, S(stream)));
+  return launch_zero_lower(reinterpret_cast<double2*>(out), r, nmat, S(stream));
+}
+
+int swsdc_download_coeffs(const double* dev, int r, long long nmat, double* host, int write_lower,
+                          void* stream) {
+  if (r < 0 || nmat < 0) { set_error("bad download arguments"); return kUsage; }
+  if (nmat == 0) return kOk;
+  void* hptr = nullptr;
+  if (cudaHostGetDevicePointer(&hptr, host, 0) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("swsdc_download_coeffs: destination is not page-locked host memory");
+    return kUsage;
+  }
+  if (write_lower) {
+    SW_CUDA(cudaMemcpyAsync(host, dev, sizeof(double2) * (size_t)nmat * (r + 1) * (r + 1),
+                            cudaMemcpyDeviceToHost, S(stream)));
+    return kOk;
+  }
+  if (download_mode() == 0)
+    return launch_download_triangle(reinterpret_cast<const double2*>(dev),
+                                    reinterpret_cast<double2*>(hptr), r, nmat, 0, S(stream));
+  // the staircase also rewrites a few lower-triangle entries with the device's zeros
+  return stair_copy(reinterpret_cast<const double2*>(dev), reinterpret_cast<double2*>(host), r, nmat,
+                    cudaMemcpyDeviceToHost, S(stream));
 }
 
 }  // extern "C"

@@ -42,6 +42,13 @@ void set_error(const std::string& msg);
     if (_s != ::swsdc::kOk) return _s;    \
   } while (0)
 
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device) and
+// size growth instead of on every launch (profile.cu).
+int set_max_dyn_smem(const void* kern, size_t smem);
+// Integer tuning knob from the environment, `dflt` when unset; callers cache it
+// in a function-local static so the environment is read once per process.
+int env_int(const char* name, int dflt);
+
 // RAII bracket of one kernel launch: counts it and, when profiling is on,
 // records CUDA events around it on `st` (profile.cu).
 class StageScope {

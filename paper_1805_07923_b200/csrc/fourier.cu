@@ -460,9 +460,7 @@ int set_smem(const void* kern, size_t smem) {
     set_error("longitude ring does not fit in shared memory (n_lon too large for this kernel)");
     return kUsage;
   }
-  if (smem > 48 * 1024)
-    SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  return kOk;
+  return set_max_dyn_smem(kern, smem);
 }
 
 // log2 of pairs per CTA: rings <= ~56 KB (4 CTAs/SM), at most 8 pairs

@@ -369,8 +369,7 @@ int launch_syn_t(const PlanDev& P, const SynArgs& a, cudaStream_t st) {
   size_t smem = sizeof(double2) * NSPLIT * B * kCS + sizeof(double) * (NSPLIT * kCS + 2);
   if (NSPLIT > 1) smem += sizeof(double2) * NSPLIT * B * kSynLat * 2;
   auto kern = syn_kernel<B, MODE, NSPLIT>;
-  if (smem > 48 * 1024)
-    SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
   StageScope sc("legendre_synthesis", st);
   kern<<<dim3(npairs, nlg, a.nmembers), NSPLIT * 32, smem, st>>>(P, a);
   SW_LAUNCH_CHECK();
@@ -606,8 +605,7 @@ template <int NT, int LSPLIT>
 int launch_ana_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st) {
   const size_t smem = sizeof(double) * kAnaWarps * (kChunk * kQS + kChunk);
   auto kern = ana_kernel<NT, LSPLIT>;
-  if (smem > 48 * 1024)
-    SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
   StageScope sc("legendre_analysis", st);
   kern<<<dim3(nwork, a.nmembers), kAnaWarps * 32, smem, st>>>(P, a);
   SW_LAUNCH_CHECK();
@@ -804,7 +802,7 @@ int launch_ana_tma(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t s
                                         kAnaWarps * (kChunk * kQS + kChunk)) +
                       sizeof(unsigned long long) * kTmaBuf + 16;
   auto kern = ana_tma_kernel<NT>;
-  SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
   StageScope sc("legendre_analysis", st);
   kern<<<dim3(nwork, a.nmembers), kAnaWarps * 32, smem, st>>>(P, a);
   SW_LAUNCH_CHECK();
@@ -819,9 +817,9 @@ int ana_warps_per_cta() { return kAnaWarps; }
 // register-prefetch kernel for wider batches, whose 16 KB tiles would limit
 // occupancy to 2 CTAs/SM.
 bool ana_uses_tma(int nv) {
-  const char* e = getenv("SWSDC_ANA_TMA");   // tuning knob: 0 = never, 2 = always
-  if (e && atoi(e) == 0) return false;
-  if (e && atoi(e) == 2) return true;
+  static const int knob = env_int("SWSDC_ANA_TMA", -1);   // tuning: 0 = never, 2 = always
+  if (knob == 0) return false;
+  if (knob == 2) return true;
   return nv <= 8;
 }
 

@@ -6,6 +6,7 @@
 // bench.py can measure each stage's device time live inside its timed region
 // (roofline "achieved").  Profiling must be off during CUDA graph capture.
 #include <atomic>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -39,6 +40,30 @@ cudaEvent_t take_event() {
 }
 
 }  // namespace
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+int set_max_dyn_smem(const void* kern, size_t smem) {
+  if (smem <= 48 * 1024) return kOk;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{kern, dev}];
+  if (have >= smem) return kOk;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    return kCuda;
+  }
+  have = smem;
+  return kOk;
+}
 
 StageScope::StageScope(const char* name, cudaStream_t st) : idx_(-1), st_(st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -9,6 +9,8 @@
 //   combine           sum_k w_k x_k (sdc.py:211-220, PrognosticState algebra swe.py:77-102)
 //   resize            truncate / pad (spharm.py:331-349)
 //   sweep_rhs         b = theta0 + sum_j c_j F_j + ... (sdc.py:185-202), fused
+#include <algorithm>
+#include <cstdlib>
 #include "common.cuh"
 #include "spectral.cuh"
 
@@ -176,6 +178,66 @@ __global__ void resize_kernel(const double2* in, int rin, double2* out, int rout
   }
 }
 
+// Host -> device upload of spectral matrices reading only the s >= r triangle
+// from page-locked host memory over PCIe (zero-copy); the lower triangle of the
+// device copy is zero-filled locally.  kUp independent loads per thread keep
+// enough PCIe read requests in flight to cover the round trip.
+constexpr int kUp = 4;
+__global__ void __launch_bounds__(256) upload_triangle_kernel(const double2* __restrict__ host,
+                                                              double2* __restrict__ out, int R,
+                                                              long long total) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < total;
+       base += stride * kUp) {
+    double2 v[kUp];
+#pragma unroll
+    for (int u = 0; u < kUp; ++u) {
+      const long long i = base + u * stride;
+      v[u] = make_double2(0.0, 0.0);
+      if (i < total) {
+        const int rs = (int)(i % ((long long)(R + 1) * (R + 1)));
+        const int r = rs / (R + 1), s = rs - r * (R + 1);
+        if (s >= r) v[u] = host[i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUp; ++u) {
+      const long long i = base + u * stride;
+      if (i < total) out[i] = v[u];
+    }
+  }
+}
+
+// Device -> host download into page-locked memory by zero-copy stores: the
+// s >= r triangle always, the (zero) lower triangle only when write_lower.
+__global__ void __launch_bounds__(256) download_triangle_kernel(const double2* __restrict__ dev,
+                                                                double2* __restrict__ host, int R,
+                                                                long long total, int write_lower) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < total;
+       base += stride * kUp) {
+    double2 v[kUp];
+    bool up[kUp];
+#pragma unroll
+    for (int u = 0; u < kUp; ++u) {
+      const long long i = base + u * stride;
+      up[u] = false;
+      v[u] = make_double2(0.0, 0.0);
+      if (i < total) {
+        const int rs = (int)(i % ((long long)(R + 1) * (R + 1)));
+        const int r = rs / (R + 1), s = rs - r * (R + 1);
+        up[u] = s >= r;
+        if (up[u]) v[u] = dev[i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUp; ++u) {
+      const long long i = base + u * stride;
+      if (i < total && (up[u] || write_lower)) host[i] = v[u];
+    }
+  }
+}
+
 __global__ void spec_combine_kernel(SpecCombineArgs a, long long nmat, RowFilter rf) {
   const int ro = a.rout;
   const long long plane = (long long)(ro + 1) * (ro + 1);
@@ -318,6 +380,52 @@ int launch_resize(const double2* in, int rin, double2* out, int rout, long long 
   const long long n = nmat * (rout + 1) * (rout + 1);
   StageScope sc("resize", st);
   resize_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, rin, out, rout, nmat, current_row_filter());
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_upload_triangle(const double2* host, double2* out, int R, long long nmat,
+                           cudaStream_t st) {
+  const long long n = nmat * (R + 1) * (R + 1);
+  StageScope sc("upload", st);
+  // PCIe needs ~(bandwidth x round trip) ~ 100-200 KB of reads in flight; 32
+  // CTAs (512 KB potential) keep the link busy while holding fewer memory-system
+  // slots against the transforms running on other streams (8 CTAs: link-bound,
+  // 64+: the concurrent transforms slow down).
+  static const int cap = std::max(1, env_int("SWSDC_UPLOAD_CTAS", 32));
+  const long long want = (n + 256LL * kUp - 1) / (256LL * kUp);
+  const int blocks = (int)std::min<long long>(want, cap);
+  upload_triangle_kernel<<<blocks, 256, 0, st>>>(host, out, R, n);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+__global__ void zero_lower_kernel(double2* out, int R, long long nmat) {
+  const long long total = nmat * (R + 1) * (R + 1);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int rs = (int)(i % ((long long)(R + 1) * (R + 1)));
+    const int r = rs / (R + 1), s = rs - r * (R + 1);
+    if (s < r) out[i] = make_double2(0.0, 0.0);
+  }
+}
+
+int launch_zero_lower(double2* out, int R, long long nmat, cudaStream_t st) {
+  const long long n = nmat * (R + 1) * (R + 1);
+  StageScope sc("zero_lower", st);
+  zero_lower_kernel<<<grid_for(n, 256), 256, 0, st>>>(out, R, nmat);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_download_triangle(const double2* dev, double2* host, int R, long long nmat,
+                             int write_lower, cudaStream_t st) {
+  const long long n = nmat * (R + 1) * (R + 1);
+  StageScope sc("download", st);
+  static const int cap = std::max(1, env_int("SWSDC_UPLOAD_CTAS", 32));
+  const long long want = (n + 256LL * kUp - 1) / (256LL * kUp);
+  const int blocks = (int)std::min<long long>(want, cap);
+  download_triangle_kernel<<<blocks, 256, 0, st>>>(dev, host, R, n, write_lower);
   SW_LAUNCH_CHECK();
   return kOk;
 }

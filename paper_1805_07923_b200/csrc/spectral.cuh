@@ -49,6 +49,11 @@ int launch_spec_combine(const SpecCombineArgs& a, long long nmat, cudaStream_t s
 // theta = solve(b, beta); fi = L_G(theta).  nstates = states per input.
 int launch_sweep_node(int R, const ModelConsts& c, double beta, const SpecCombineArgs& a,
                       double2* theta, double2* fi, long long nstates, cudaStream_t st);
+int launch_upload_triangle(const double2* host, double2* out, int R, long long nmat,
+                           cudaStream_t st);
+int launch_download_triangle(const double2* dev, double2* host, int R, long long nmat,
+                             int write_lower, cudaStream_t st);
+int launch_zero_lower(double2* out, int R, long long nmat, cudaStream_t st);
 int launch_resize(const double2* in, int rin, double2* out, int rout, long long nmat,
                   cudaStream_t st);
 

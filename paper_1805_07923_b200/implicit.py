@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _lib, spharm
-from .spharm import _ptr, _stream_ptr
+from .spharm import _dev_guard, _ptr, _stream_ptr
 from .swe import ModelParams, PrognosticState
 
 
@@ -49,7 +49,7 @@ def solve_implicit(b: PrognosticState, ctx: ImplicitSolveContext) -> PrognosticS
     out = torch.empty_like(x)
     nmat = int(np.prod(x.shape[:-3])) if x.dim() > 3 else 1
     cp = _lib.params_struct(ctx.params)
-    with torch.cuda.device(x.device):
+    with _dev_guard(x.device):
         _lib.check(_lib.load().swsdc_solve_implicit(R, ctypes.byref(cp), beta, _ptr(x), nmat,
                                                     _ptr(out), _stream_ptr(x.device)))
     return PrognosticState.from_tensor(out)

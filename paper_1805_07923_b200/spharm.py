@@ -16,7 +16,9 @@ everything per transform is CUDA.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import math
 import dataclasses
 
 import numpy as np
@@ -150,16 +152,88 @@ def _to_device(x, dtype, device):
     return torch.from_numpy(arr).to(device), True
 
 
+def _is_pinned_host(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.device.type == "cpu" and x.is_pinned()
+
+
+def upload_coeffs(host: torch.Tensor, out: torch.Tensor | None = None, device=None) -> torch.Tensor:
+    """Page-locked host coefficients (..., R+1, R+1) complex128 -> device tensor.
+
+    Only the s >= r triangle that the reference layout populates crosses PCIe
+    (a zero-copy kernel, half the bytes of a dense copy); the device copy's lower
+    triangle is zero.  Asynchronous on the current stream, like
+    `Tensor.to(non_blocking=True)`."""
+    if not _is_pinned_host(host):
+        raise ValueError("upload_coeffs needs a page-locked (pinned) host tensor")
+    if host.dtype != torch.complex128 or not host.is_contiguous():
+        raise ValueError("upload_coeffs needs a contiguous complex128 tensor")
+    if host.dim() < 2 or host.shape[-1] != host.shape[-2]:
+        raise ValueError(f"coefficient array of shape {tuple(host.shape)} is not (..., R+1, R+1)")
+    device = torch.device(device) if device is not None else (
+        out.device if out is not None else torch.device("cuda", torch.cuda.current_device()))
+    if out is None:
+        out = torch.empty(host.shape, dtype=torch.complex128, device=device)
+    elif out.shape != host.shape or out.dtype != torch.complex128 or not out.is_contiguous():
+        raise ValueError("out has the wrong shape or layout")
+    R = host.shape[-1] - 1
+    nmat = host.numel() // ((R + 1) * (R + 1))
+    with _dev_guard(out.device):
+        _lib.check(_lib.load().swsdc_upload_coeffs(_ptr(host), R, nmat, _ptr(out),
+                                                   _stream_ptr(out.device)))
+    return out
+
+
+def download_coeffs(dev: torch.Tensor, out: torch.Tensor, write_lower: bool = True) -> torch.Tensor:
+    """Device coefficients (..., R+1, R+1) -> page-locked host tensor `out` by the
+    copy engine, asynchronous on the current stream.  write_lower=False sends
+    (about) only the s >= r triangle, half the PCIe bytes: entries of `out` below
+    it are either left untouched or receive the device's values -- for results
+    streamed into a reused, zero-initialised buffer, where they stay zero."""
+    if not _is_pinned_host(out):
+        raise ValueError("download_coeffs needs a page-locked (pinned) host `out`")
+    if (dev.dtype != torch.complex128 or out.dtype != torch.complex128 or not dev.is_cuda
+            or not dev.is_contiguous() or not out.is_contiguous() or dev.shape != out.shape):
+        raise ValueError("download_coeffs needs contiguous complex128 tensors of one shape")
+    if dev.dim() < 2 or dev.shape[-1] != dev.shape[-2]:
+        raise ValueError(f"coefficient array of shape {tuple(dev.shape)} is not (..., R+1, R+1)")
+    R = dev.shape[-1] - 1
+    nmat = dev.numel() // ((R + 1) * (R + 1))
+    with _dev_guard(dev.device):
+        _lib.check(_lib.load().swsdc_download_coeffs(_ptr(dev), R, nmat, _ptr(out),
+                                                     1 if write_lower else 0,
+                                                     _stream_ptr(dev.device)))
+    return out
+
+
 def _out(t: torch.Tensor, host: bool):
     return t.cpu().numpy() if host else t
 
 
-def _stream_ptr(device) -> ctypes.c_void_p:
-    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 
 
-def _ptr(t: torch.Tensor) -> ctypes.c_void_p:
-    return ctypes.c_void_p(t.data_ptr())
+def _stream_ptr(device) -> int:
+    """Raw cudaStream_t of the current stream on `device` (an int: ctypes converts
+    it for c_void_p arguments); the cheap path avoids building a Stream object,
+    which dominated the host cost of small calls."""
+    idx = device.index
+    if idx is None:
+        idx = torch.cuda.current_device()
+    if _raw_stream is not None:
+        return _raw_stream(idx)
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+def _dev_guard(device):
+    """Make `device` current for the library's launches; a no-op (no context
+    switch) when it already is."""
+    if device.index is None or device.index == torch.cuda.current_device():
+        return contextlib.nullcontext()
+    return torch.cuda.device(device)
 
 
 class TransformPlan:
@@ -185,7 +259,7 @@ class TransformPlan:
         mu = np.ascontiguousarray(grid.mu, dtype=np.float64)
         w = np.ascontiguousarray(grid.w, dtype=np.float64)
         handle = ctypes.c_void_p()
-        with torch.cuda.device(self.device):
+        with _dev_guard(self.device):
             _lib.check(lib.swsdc_plan_create(
                 truncation, grid.n_lon, grid.n_lat, mu.ctypes.data_as(ctypes.c_void_p),
                 w.ctypes.data_as(ctypes.c_void_p), ctypes.byref(handle)))
@@ -208,7 +282,7 @@ class TransformPlan:
 
     def reserve(self, fields: int) -> None:
         """Pre-size the scratch workspace (needed before CUDA graph capture)."""
-        with torch.cuda.device(self.device):
+        with _dev_guard(self.device):
             _lib.check(self._lib.swsdc_plan_reserve(self._handle, int(fields)))
 
     # -- shape helpers ------------------------------------------------------
@@ -222,7 +296,11 @@ class TransformPlan:
         return t, host
 
     def _coeff_in(self, coeffs):
-        t, host = _to_device(coeffs, torch.complex128, self.device)
+        if (_is_pinned_host(coeffs) and coeffs.dtype == torch.complex128 and coeffs.is_contiguous()
+                and coeffs.dim() >= 2 and coeffs.shape[-1] == coeffs.shape[-2]):
+            t, host = upload_coeffs(coeffs, device=self.device), False
+        else:
+            t, host = _to_device(coeffs, torch.complex128, self.device)
         if t.dim() < 2 or t.shape[-1] != t.shape[-2]:
             raise ValueError(f"coefficient array of shape {tuple(t.shape)} is not (..., R+1, R+1)")
         r_in = t.shape[-1] - 1
@@ -235,18 +313,29 @@ class TransformPlan:
     # -- public transforms (spharm.py:254-300) ------------------------------
     def analyze(self, field, out: torch.Tensor | None = None):
         """Grid field (..., n_lon, n_lat) -> coefficients (..., R+1, R+1).
-        `out` (optional, CUDA, contiguous) receives the result in place."""
+        `out` (optional, contiguous complex128) receives the result in place: a CUDA
+        tensor, or a page-locked host tensor filled by an asynchronous copy on the
+        current stream (synchronize before reading it)."""
         g, host = self._grid_in(field)
         lead = g.shape[:-2]
-        nb = int(np.prod(lead)) if lead else 1
+        nb = math.prod(lead)
         R = self.truncation
+        target = out
+        if out is not None and (tuple(out.shape) != tuple(lead) + (R + 1, R + 1)
+                                or not out.is_contiguous() or out.dtype != torch.complex128):
+            raise ValueError("out has the wrong shape or layout")
+        if out is not None and out.device.type == "cpu":
+            if not out.is_pinned():
+                raise ValueError("a host `out` must be page-locked (pinned)")
+            out = None
         if out is None:
             out = torch.empty(lead + (R + 1, R + 1), dtype=torch.complex128, device=self.device)
-        elif tuple(out.shape) != tuple(lead) + (R + 1, R + 1) or not out.is_contiguous():
-            raise ValueError("out has the wrong shape or layout")
-        with torch.cuda.device(self.device):
+        with _dev_guard(self.device):
             _lib.check(self._lib.swsdc_analyze(self._handle, _ptr(g), nb, _ptr(out),
                                                _stream_ptr(self.device)))
+            if target is not None and target.device.type == "cpu":
+                target.copy_(out, non_blocking=True)
+                return target
         return _out(out, host)
 
     def synthesize(self, coeffs, out: torch.Tensor | None = None):
@@ -254,13 +343,13 @@ class TransformPlan:
         `out` (optional, CUDA, contiguous) receives the result in place."""
         c, host, r_in = self._coeff_in(coeffs)
         lead = c.shape[:-2]
-        nb = int(np.prod(lead)) if lead else 1
+        nb = math.prod(lead)
         shape = tuple(lead) + (self.grid.n_lon, self.grid.n_lat)
         if out is None:
             out = torch.empty(shape, dtype=torch.float64, device=self.device)
         elif tuple(out.shape) != shape or not out.is_contiguous():
             raise ValueError("out has the wrong shape or layout")
-        with torch.cuda.device(self.device):
+        with _dev_guard(self.device):
             _lib.check(self._lib.swsdc_synthesize(self._handle, _ptr(c), r_in, nb, _ptr(out),
                                                   _stream_ptr(self.device)))
         return _out(out, host)
@@ -272,11 +361,11 @@ class TransformPlan:
         if p.shape != c.shape:
             raise ValueError("psi and chi must share one shape")
         lead = p.shape[:-2]
-        nb = int(np.prod(lead)) if lead else 1
+        nb = math.prod(lead)
         shape = lead + (self.grid.n_lon, self.grid.n_lat)
         u = torch.empty(shape, dtype=torch.float64, device=self.device)
         v = torch.empty(shape, dtype=torch.float64, device=self.device)
-        with torch.cuda.device(self.device):
+        with _dev_guard(self.device):
             _lib.check(self._lib.swsdc_synthesize_uv(self._handle, _ptr(p), _ptr(c), r_in, nb,
                                                      _ptr(u), _ptr(v), _stream_ptr(self.device)))
         return _out(u, host), _out(v, host)
@@ -288,11 +377,11 @@ class TransformPlan:
         if u.shape != v.shape:
             raise ValueError("cos_u and cos_v must share one shape")
         lead = u.shape[:-2]
-        nb = int(np.prod(lead)) if lead else 1
+        nb = math.prod(lead)
         R = self.truncation
         div = torch.empty(lead + (R + 1, R + 1), dtype=torch.complex128, device=self.device)
         curl = torch.empty_like(div)
-        with torch.cuda.device(self.device):
+        with _dev_guard(self.device):
             _lib.check(self._lib.swsdc_analyze_divcurl(self._handle, _ptr(u), _ptr(v), nb,
                                                        _ptr(div), _ptr(curl),
                                                        _stream_ptr(self.device)))
@@ -346,10 +435,10 @@ def _resize(coeffs, r_out: int):
     c, host = _to_device(coeffs, torch.complex128, _dev_of(coeffs))
     r_in = c.shape[-1] - 1
     lead = c.shape[:-2]
-    nmat = int(np.prod(lead)) if lead else 1
+    nmat = math.prod(lead)
     out = torch.empty(lead + (r_out + 1, r_out + 1), dtype=torch.complex128, device=c.device)
     lib = _lib.load()
-    with torch.cuda.device(c.device):
+    with _dev_guard(c.device):
         _lib.check(lib.swsdc_resize(_ptr(c), r_in, _ptr(out), r_out, nmat, _stream_ptr(c.device)))
     return _out(out, host)
 

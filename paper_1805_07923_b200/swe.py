@@ -13,13 +13,14 @@ incremented exactly where the reference increments them (swe.py:248, 257,
 from __future__ import annotations
 
 import ctypes
+import math
 import dataclasses
 
 import numpy as np
 import torch
 
 from . import _lib, spharm
-from .spharm import TransformPlan, _ptr, _stream_ptr, _to_device
+from .spharm import TransformPlan, _dev_guard, _ptr, _stream_ptr, _to_device
 
 
 @dataclasses.dataclass(frozen=True)
@@ -61,7 +62,7 @@ def combine(weights, tensors, out: torch.Tensor | None = None) -> torch.Tensor:
     n = len(pairs)
     ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() for _, t in pairs])
     ws = (ctypes.c_double * n)(*[w for w, _ in pairs])
-    with torch.cuda.device(ref.device):
+    with _dev_guard(ref.device):
         _lib.check(lib.swsdc_combine(n, ptrs, ws, ref.numel() * 2, _ptr(out),
                                      _stream_ptr(ref.device)))
     return out
@@ -87,8 +88,8 @@ def spec_combine(weights, tensors, r_out: int, out: torch.Tensor | None = None) 
     ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() for _, t in pairs])
     ws = (ctypes.c_double * n)(*[w for w, _ in pairs])
     rin = (ctypes.c_int * n)(*[t.shape[-1] - 1 for _, t in pairs])
-    nmat = int(np.prod(lead)) if lead else 1
-    with torch.cuda.device(ref.device):
+    nmat = math.prod(lead)
+    with _dev_guard(ref.device):
         _lib.check(_lib.load().swsdc_spec_combine(n, ptrs, ws, rin, r_out, nmat, _ptr(out),
                                                   _stream_ptr(ref.device)))
     return out
@@ -269,7 +270,7 @@ class ShallowWaterRHS:
         self._check(state)
         x = state.data.contiguous()
         out = torch.empty_like(x)
-        with torch.cuda.device(x.device):
+        with _dev_guard(x.device):
             _lib.check(_lib.load().swsdc_eval_fi(self.truncation, ctypes.byref(self._cparams),
                                                  _ptr(x), self._nmat(state), _ptr(out),
                                                  _stream_ptr(x.device)))
@@ -279,7 +280,7 @@ class ShallowWaterRHS:
         self._check(state)
         x = state.data.contiguous()
         out = torch.empty_like(x)
-        with torch.cuda.device(x.device):
+        with _dev_guard(x.device):
             _lib.check(_lib.load().swsdc_eval_fe(self.plan.handle, ctypes.byref(self._cparams),
                                                  1 if nonlinear else 0, _ptr(x), self._nmat(state),
                                                  _ptr(out), _stream_ptr(x.device)))
@@ -326,7 +327,7 @@ class ShallowWaterRHS:
         ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() for _, t in pairs])
         ws = (ctypes.c_double * n)(*[w for w, _ in pairs])
         nmat = int(np.prod(ref.shape[:-3])) if ref.dim() > 3 else 1
-        with torch.cuda.device(ref.device):
+        with _dev_guard(ref.device):
             _lib.check(_lib.load().swsdc_sweep_node(self.truncation, ctypes.byref(self._cparams),
                                                     float(beta), n, ptrs, ws, nmat, _ptr(theta),
                                                     _ptr(fi), _stream_ptr(ref.device)))

@@ -70,3 +70,42 @@ def test_batched_transforms_match_oracle():
     want_b = np.stack([oplan.analyze(gi) for gi in want])
     assert rel_err(back.cpu().numpy(), want_b) < TOL
     assert rel_err(back.cpu().numpy(), c) < TOL
+
+
+def test_pinned_host_upload_and_download(golden):
+    """synthesize() of a pinned host tensor uploads only the s >= r triangle (the
+    lower triangle, garbage here, must not be read) and analyze(out=pinned host)
+    copies the result back; both equal the device-resident path bit for bit."""
+    from paper_1805_07923_b200 import spharm
+    R, I, J = 31, 96, 48
+    plan = plan_for(R, I, J)
+    c = np.stack([golden[f"R{R}_I{I}_J{J}_c"]] * 3)
+    dirty = c.copy()
+    lo = np.tril_indices(R + 1, -1)
+    dirty[:, lo[0], lo[1]] = 1e300 + 7j
+    host = torch.from_numpy(dirty).pin_memory()
+    dev = spharm.upload_coeffs(host)
+    torch.cuda.synchronize()
+    assert np.array_equal(dev.cpu().numpy(), c)
+    g_ref = plan.synthesize(torch.from_numpy(c).cuda())
+    g_host = plan.synthesize(host)
+    assert g_host.is_cuda and torch.equal(g_ref, g_host)
+    o_pin = torch.empty(c.shape, dtype=torch.complex128).pin_memory()
+    assert plan.analyze(g_ref, out=o_pin) is o_pin
+    torch.cuda.synchronize()
+    assert torch.equal(o_pin, plan.analyze(g_ref).cpu())
+    sentinel = torch.full(c.shape, 3 + 4j, dtype=torch.complex128).pin_memory()
+    spharm.download_coeffs(dev, sentinel, write_lower=False)
+    dense = torch.full(c.shape, 3 + 4j, dtype=torch.complex128).pin_memory()
+    spharm.download_coeffs(dev, dense)
+    torch.cuda.synchronize()
+    assert np.array_equal(dense.numpy(), c)
+    tri = np.triu_indices(R + 1)
+    assert np.array_equal(sentinel.numpy()[:, tri[0], tri[1]], c[:, tri[0], tri[1]])
+    below = sentinel.numpy()[:, lo[0], lo[1]]
+    assert np.all((below == 3 + 4j) | (below == 0))      # untouched, or the device's zeros
+    assert np.mean(below == 3 + 4j) > 0.5                # ... and mostly not sent at all
+    with pytest.raises(ValueError):
+        spharm.upload_coeffs(torch.from_numpy(c))          # pageable: refused
+    with pytest.raises(ValueError):
+        plan.analyze(g_ref, out=torch.empty(c.shape, dtype=torch.complex128))
