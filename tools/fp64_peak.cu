@@ -82,7 +82,7 @@ int main() {
   double* out; CK(cudaMalloc(&out, 1 << 20));
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   printf("SMs %d\n", sms);
-  for (int occ : {4, 8, 16}) {
+  for (int occ : {1, 2, 3, 4, 8, 16}) {
     int blocks = sms * occ, threads = 128;
     float ms = timeit(k_dfma, blocks, threads, out);
     double fl = 2.0 * 8 * ITERS * (double)blocks * threads;
