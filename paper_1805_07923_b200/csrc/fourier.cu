@@ -27,6 +27,7 @@
 
 #include "common.cuh"
 #include "fourier.cuh"
+#include "reg_fft.cuh"
 
 namespace swsdc {
 namespace {
@@ -267,6 +268,171 @@ __global__ void __launch_bounds__(256, 2) g2f_kernel(PlanDev P, const double* gr
 }
 
 // ---------------------------------------------------------------------------
+// Register-FFT variants (n_lon = 32 K, reg_fft.cuh): warp w of the CTA owns
+// ring w.  Shared memory only carries the coalesced grid loads/stores and the
+// analysis-layout writes (rings in natural order, padded); the transforms run
+// in registers with no CTA barriers between stages.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// E/O staging row stride (double2) for np pairs: 2 np + 1 keeps the lanes'
+// reads of consecutive wavenumbers in distinct bank groups.
+__host__ __device__ inline int eo_row(int np) { return 2 * np + 1; }
+
+// K >= 16: 4 pairs (128 threads) per CTA, registers capped for 3 CTAs/SM;
+// smaller rings: up to 8 pairs (256 threads).
+#define SWSDC_REG_BOUNDS(K) __launch_bounds__((K) >= 16 ? 128 : 256, (K) >= 16 ? 3 : 2)
+
+template <int K>
+__global__ void SWSDC_REG_BOUNDS(K) f2g_reg_kernel(PlanDev P, const double2* eo,
+                                                      long long eo_fstride, double* grid,
+                                                      long long grid_fstride, int lnp,
+                                                      int jh_begin, int jh_end) {
+  extern __shared__ __align__(16) double2 rings[];
+  const int np = 1 << lnp;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int f = blockIdx.y;
+  const int jh0 = jh_begin + blockIdx.x * np;
+  const int R = P.R, I = P.I, row = eo_row(np);
+  // 1. stage the CTA's (E, O) rows with async copies: for each r, np pairs x
+  //    (E, O) = 32 np contiguous bytes; every copy is in flight at once
+  {
+    const double2* e = eo + (size_t)f * eo_fstride;
+    const int per_r = 2 * np, total = (R + 1) * per_r;
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+      const int r = idx >> (lnp + 1), c = idx & (per_r - 1);   // c = 2 i + (E|O)
+      const int jh = jh0 + (c >> 1);
+      double2* dst = rings + (size_t)r * row + c;
+      if (jh < jh_end) cp_async16(dst, e + ((size_t)r * P.Jh + jh) * 2 + (c & 1));
+      else *dst = d2(0.0, 0.0);
+    }
+    cp_async_wait_all();
+  }
+  __syncthreads();
+  // 2. each warp assembles its pair's packed spectrum in registers and transforms it
+  const int jhw = jh0 + warp;
+  double2 v[K];
+  double2 wst[3];
+  swfft::cross_twiddles<K, true>(wst, P.tw, lane);
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int n = 32 * k + lane;
+    const bool lo = n <= R, hi = n >= I - R;
+    const int r = lo ? n : I - n;
+    v[k] = d2(0.0, 0.0);
+    if (lo || hi) {
+      const double2* src = rings + (size_t)r * row + 2 * warp;
+      double2 zp, zm;
+      pair_spectrum(src[0], src[1], r, zp, zm);
+      v[k] = lo ? zp : zm;
+    }
+  }
+  __syncthreads();   // staging consumed; the rings reuse its space
+  if (jhw < jh_end) {
+    swfft::ring_fft<K, true>(v, P.tw, lane, wst);
+    double2* ring = rings + (size_t)warp * P.ring_stride;
+#pragma unroll
+    for (int m1 = 0; m1 < K; ++m1) ring[swfft::pad_idx(swfft::ring_out_index<K>(lane, m1))] = v[m1];
+  }
+  __syncthreads();
+  {
+    // thread -> fixed pair i, longitudes il0, il0 + step, ...: np consecutive
+    // threads write np consecutive latitudes of one longitude row
+    const int i = threadIdx.x & (np - 1), step = blockDim.x >> lnp;
+    const int jh = jh0 + i;
+    if (jh < jh_end) {
+      const int jn = jn_of(P, jh), js = js_of(P, jh);
+      double* gn = grid + (size_t)f * grid_fstride + jn;
+      const long long dj = (long long)(js - jn);
+      const double2* ring = rings + (size_t)i * P.ring_stride;
+      for (int il = threadIdx.x >> lnp; il < P.I; il += step) {
+        const double2 z = ring[swfft::pad_idx(il)];
+        double* gp = gn + (size_t)il * P.J;
+        gp[0] = z.x;
+        if (dj != 0) gp[dj] = z.y;
+      }
+    }
+  }
+}
+
+template <int K, int MODE>
+__global__ void SWSDC_REG_BOUNDS(K) g2f_reg_kernel(PlanDev P, const double* grid,
+                                                      const double* grid2, long long grid_fstride,
+                                                      double* x, XLayout xl, int lnp) {
+  constexpr int NIN = (MODE == 0) ? 1 : 2;
+  extern __shared__ __align__(16) double2 rings[];  // [NIN][np][RS], natural order
+  const int np = 1 << lnp;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int f = blockIdx.y;
+  const int jh0 = blockIdx.x * np;
+  const double* gin[2] = {grid + (size_t)f * grid_fstride,
+                          (MODE == 0 ? grid : grid2) + (size_t)f * grid_fstride};
+  {
+    // async 8-byte copies straight into the natural-order rings: thread ->
+    // fixed (ring q, pair i, side) slot, strided over longitudes; 2 np
+    // consecutive threads read 2 x np consecutive latitudes of one row
+    const int nslot = 2 * np * NIN, slot = threadIdx.x % nslot, step = blockDim.x / nslot;
+    const int q = slot / (2 * np), c = slot - q * 2 * np, i = c >> 1, side = c & 1;
+    const int jh = jh0 + i;
+    double* dst0 = reinterpret_cast<double*>(rings + (size_t)(q * np + i) * P.ring_stride) + side;
+    if (jh < P.Jh) {
+      const double* src0 = gin[q] + (side ? js_of(P, jh) : jn_of(P, jh));
+      for (int il = threadIdx.x / nslot; il < P.I; il += step)
+        cp_async8(dst0 + 2 * swfft::pad_idx(il), src0 + (size_t)il * P.J);
+    } else {
+      for (int il = threadIdx.x / nslot; il < P.I; il += step) dst0[2 * swfft::pad_idx(il)] = 0.0;
+    }
+    cp_async_wait_all();
+  }
+  __syncthreads();
+  {
+    // warp w transforms ring w (q = w / np, pair w % np)
+    double2 wst[3];
+    swfft::cross_twiddles<K, false>(wst, P.tw, lane);
+    double2* ring = rings + (size_t)warp * P.ring_stride;
+    double2 v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
+    swfft::ring_fft<K, false>(v, P.tw, lane, wst);
+    __syncwarp();
+#pragma unroll
+    for (int m1 = 0; m1 < K; ++m1) ring[swfft::pad_idx(swfft::ring_out_index<K>(lane, m1))] = v[m1];
+  }
+  __syncthreads();
+  double* xf = x + (MODE == 0 ? 0 : (size_t)f * xl.mstride);
+  for (int idx = threadIdx.x; idx < ((P.R + 1) << lnp); idx += blockDim.x) {
+    const int r = idx >> lnp, i = idx & (np - 1);
+    const int jh = jh0 + i;
+    if (jh >= P.Jh) continue;
+    const bool eq = (jn_of(P, jh) == js_of(P, jh));
+    const double mu = P.mu_n[jh], w = P.w_n[jh];
+    if (MODE == 0) {
+      double2 Fn, Fs;
+      get_pair(rings + (size_t)i * P.ring_stride, P, r, Fn, Fs);
+      put_x(xf, xl, f, r, jh, cscale(Fn, w), cscale(Fs, w), eq);
+    } else {
+      double2 Un, Us, Vn, Vs;
+      get_pair(rings + (size_t)i * P.ring_stride, P, r, Un, Us);
+      get_pair(rings + (size_t)(np + i) * P.ring_stride, P, r, Vn, Vs);
+      const double wc = w / (1.0 - mu * mu);
+      const double rw = r * wc;
+      put_x(xf, xl, 0, r, jh, ir_scale(Un, rw), ir_scale(Us, rw), eq);
+      put_x(xf, xl, 1, r, jh, cscale(Vn, -wc), cscale(Vs, -wc), eq);
+      put_x(xf, xl, 2, r, jh, ir_scale(Vn, rw), ir_scale(Vs, rw), eq);
+      put_x(xf, xl, 3, r, jh, cscale(Un, wc), cscale(Us, wc), eq);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Fused explicit-tendency grid stage, one latitude pair per CTA.
 //   in : eo[m][5][R+1][Jh][2] for (U/a, V/a, zeta, delta, phi')
 //   out: x[m][NV][R+1][Jh][2], NV = 7 (nonlinear) or 2 (linear only)
@@ -471,6 +637,59 @@ int pairs_log2(const PlanDev& P, int nin) {
   return l;
 }
 
+// Register-FFT dispatch: n_lon = 32 K with K in reg_fft_k_ok (SWSDC_REG_FFT=0 disables).
+bool use_reg_fft(const PlanDev& P) {
+  static const int knob = env_int("SWSDC_REG_FFT", 1);
+  return knob != 0 && P.I % 32 == 0 && swfft::reg_fft_k_ok(P.I / 32);
+}
+
+template <int K>
+int f2g_reg_launch(const PlanDev& P, const double2* eo, long long eo_fstride, double* grid,
+                   long long grid_fstride, int nf, int jh_begin, int jh_end, cudaStream_t st) {
+  const int lnp = pairs_log2(P, 1), np = 1 << lnp;
+  const size_t smem = sizeof(double2) * std::max((size_t)np * P.ring_stride,
+                                                 (size_t)(P.R + 1) * eo_row(np));
+  SW_TRY(set_smem((const void*)f2g_reg_kernel<K>, smem));
+  dim3 gridDim((jh_end - jh_begin + np - 1) / np, nf);
+  if (gridDim.x == 0) return kOk;
+  StageScope sc("fourier_to_grid", st);
+  f2g_reg_kernel<K><<<gridDim, 32 * np, smem, st>>>(P, eo, eo_fstride, grid, grid_fstride, lnp,
+                                                   jh_begin, jh_end);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+template <int K, int MODE>
+int g2f_reg_launch(const PlanDev& P, const double* grid, const double* grid2,
+                   long long grid_fstride, double* x, const XLayout& xl, int nf, cudaStream_t st) {
+  const int nin = MODE == 0 ? 1 : 2;
+  const int lnp = std::min(pairs_log2(P, nin), 3 - (nin - 1)), np = 1 << lnp;   // <= 8 warps
+  const size_t smem = sizeof(double2) * nin * np * P.ring_stride;
+  dim3 gridDim((P.Jh + np - 1) / np, nf);
+  SW_TRY(set_smem((const void*)g2f_reg_kernel<K, MODE>, smem));
+  StageScope sc(MODE == 0 ? "grid_to_fourier" : "grid_to_fourier_divcurl", st);
+  g2f_reg_kernel<K, MODE><<<gridDim, 32 * nin * np, smem, st>>>(P, grid, grid2, grid_fstride, x,
+                                                               xl, lnp);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+#define SWSDC_REG_K_SWITCH(K_, CALL)                                              \
+  switch (K_) {                                                                   \
+    case 1: { constexpr int KK = 1; return CALL; }                                \
+    case 2: { constexpr int KK = 2; return CALL; }                                \
+    case 3: { constexpr int KK = 3; return CALL; }                                \
+    case 4: { constexpr int KK = 4; return CALL; }                                \
+    case 5: { constexpr int KK = 5; return CALL; }                                \
+    case 6: { constexpr int KK = 6; return CALL; }                                \
+    case 8: { constexpr int KK = 8; return CALL; }                                \
+    case 10: { constexpr int KK = 10; return CALL; }                              \
+    case 12: { constexpr int KK = 12; return CALL; }                              \
+    case 16: { constexpr int KK = 16; return CALL; }                              \
+    case 20: { constexpr int KK = 20; return CALL; }                              \
+    case 24: { constexpr int KK = 24; return CALL; }                              \
+  }
+
 template <bool BIGP>
 int f2g_launch(const PlanDev& P, const double2* eo, long long eo_fstride, double* grid,
                long long grid_fstride, int nf, int jh_begin, int jh_end, cudaStream_t st) {
@@ -561,6 +780,10 @@ int launch_fourier_to_grid(const PlanDev& P, const double2* eo, long long eo_fst
                            long long grid_fstride, int nf, cudaStream_t st, int jh_begin,
                            int jh_end) {
   if (jh_end < 0) jh_end = P.Jh;
+  if (use_reg_fft(P)) {
+    SWSDC_REG_K_SWITCH(P.I / 32, (f2g_reg_launch<KK>(P, eo, eo_fstride, grid, grid_fstride, nf,
+                                                     jh_begin, jh_end, st)));
+  }
   if (swfft::fft_needs_bigp(P.I))
     return f2g_launch<true>(P, eo, eo_fstride, grid, grid_fstride, nf, jh_begin, jh_end, st);
   return f2g_launch<false>(P, eo, eo_fstride, grid, grid_fstride, nf, jh_begin, jh_end, st);
@@ -569,6 +792,13 @@ int launch_fourier_to_grid(const PlanDev& P, const double2* eo, long long eo_fst
 int launch_grid_to_fourier(const PlanDev& P, int mode, const double* grid, const double* grid2,
                            long long grid_fstride, double* x, const XLayout& xl, int nf,
                            cudaStream_t st) {
+  if (use_reg_fft(P)) {
+    if (mode == 0) {
+      SWSDC_REG_K_SWITCH(P.I / 32, (g2f_reg_launch<KK, 0>(P, grid, grid2, grid_fstride, x, xl, nf, st)));
+    } else {
+      SWSDC_REG_K_SWITCH(P.I / 32, (g2f_reg_launch<KK, 1>(P, grid, grid2, grid_fstride, x, xl, nf, st)));
+    }
+  }
   const bool big = swfft::fft_needs_bigp(P.I);
   if (mode == 0) {
     if (big) return g2f_launch<0, true>(P, grid, grid2, grid_fstride, x, xl, nf, st);

@@ -1,0 +1,182 @@
+// Register-resident complex FFT of one ring of N = 32 K points per warp.
+//
+// Lane l holds x[32 k + l] in v[k] (k < K).  With m = m1 + K m2,
+//   X[m] = sum_l W_32^(l m2) W_N^(l m1) sum_k x[32 k + l] W_K^(k m1),
+// so the transform is (A) a K-point DFT over the lane's own registers,
+// (B) the twiddle W_N^(l m1) on slot m1, (C) a 32-point DFT across the lanes
+// (radix-2 decimation in frequency over shfl.xor).  Afterwards lane l holds
+// X[m1 + K brev5(l)] in v[m1].  No shared memory and no barriers: the only
+// latency is the shuffles', and every stage has K independent chains.
+//
+// Twiddles come from the plan table tw[e] = exp(-2 pi i e / N) (capi.cu),
+// conjugated for the inverse: W_K^e = tw[32 e], W_32^e = tw[K e].
+#pragma once
+
+#include "fft_core.cuh"
+
+namespace swfft {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ double2 tw_at(const double2* tw, int e, bool inverse) {
+  double2 w = tw[e];
+  if (inverse) w.y = -w.y;
+  return w;
+}
+
+// W_K^e (conjugated for the inverse) for K dividing 24 or 20, as compile-time
+// constants: inside the unrolled DFTs e is a constant, so these fold into
+// immediates instead of table loads.
+template <int K, bool INV>
+__device__ __forceinline__ double2 wk(int e) {
+  constexpr double h = 0.70710678118654752440, r3 = 0.86602540378443864676;
+  constexpr double a15 = 0.96592582628906828675, b15 = 0.25881904510252076235;
+  if constexpr (24 % K == 0) {
+    constexpr double c[24] = {1.0, a15, r3, h, 0.5, b15, 0.0, -b15, -0.5, -h, -r3, -a15,
+                              -1.0, -a15, -r3, -h, -0.5, -b15, 0.0, b15, 0.5, h, r3, a15};
+    constexpr double s[24] = {0.0, -b15, -0.5, -h, -r3, -a15, -1.0, -a15, -r3, -h, -0.5, -b15,
+                              0.0, b15, 0.5, h, r3, a15, 1.0, a15, r3, h, 0.5, b15};
+    const int i = (e * (24 / K)) % 24;
+    return mk2(c[i], INV ? -s[i] : s[i]);
+  } else {
+    static_assert(20 % K == 0, "twiddle constants cover K | 24 and K | 20");
+    constexpr double c1 = 0.95105651629515357212, s1 = 0.30901699437494742410;
+    constexpr double c2 = 0.80901699437494742410, s2 = 0.58778525229247312917;
+    constexpr double c[20] = {1.0, c1, c2, s2, s1, 0.0, -s1, -s2, -c2, -c1,
+                              -1.0, -c1, -c2, -s2, -s1, 0.0, s1, s2, c2, c1};
+    constexpr double s[20] = {0.0, -s1, -s2, -c2, -c1, -1.0, -c1, -c2, -s2, -s1,
+                              0.0, s1, s2, c2, c1, 1.0, c1, c2, s2, s1};
+    const int i = (e * (20 / K)) % 20;
+    return mk2(c[i], INV ? -s[i] : s[i]);
+  }
+}
+
+// K = A * B: A-point DFTs over stride-B subsequences, twiddles W_K^(kb ma),
+// B-point DFTs; natural order in and out.
+template <int A, int B, bool INV>
+__device__ __forceinline__ void dft_ab(double2* v, const double2* tw) {
+  double2 t[A * B];
+#pragma unroll
+  for (int kb = 0; kb < B; ++kb) {
+    double2 a[A];
+#pragma unroll
+    for (int ka = 0; ka < A; ++ka) a[ka] = v[B * ka + kb];
+    small_dft<A>(a, INV);
+#pragma unroll
+    for (int ma = 0; ma < A; ++ma) {
+      double2 z = a[out_slot<A>(ma)];
+      if (kb * ma != 0) z = cmul(z, wk<A * B, INV>(kb * ma));
+      t[kb * A + ma] = z;
+    }
+  }
+#pragma unroll
+  for (int ma = 0; ma < A; ++ma) {
+    double2 b[B];
+#pragma unroll
+    for (int kb = 0; kb < B; ++kb) b[kb] = t[kb * A + ma];
+    small_dft<B>(b, INV);
+#pragma unroll
+    for (int mb = 0; mb < B; ++mb) v[ma + A * mb] = b[out_slot<B>(mb)];
+  }
+}
+
+// K-point DFT in registers, natural order in and out.
+template <int K, bool INV>
+__device__ __forceinline__ void dft_k(double2* v, const double2* tw) {
+  if constexpr (K == 1) {
+  } else if constexpr (K == 2 || K == 3 || K == 4 || K == 5 || K == 8) {
+    small_dft<K>(v, INV);
+  } else if constexpr (K == 16) {
+    small_dft<16>(v, INV);
+    double2 t[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) t[q] = v[out_slot<16>(q)];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = t[q];
+  } else if constexpr (K == 6) {
+    dft_ab<3, 2, INV>(v, tw);
+  } else if constexpr (K == 10) {
+    dft_ab<5, 2, INV>(v, tw);
+  } else if constexpr (K == 12) {
+    dft_ab<3, 4, INV>(v, tw);
+  } else if constexpr (K == 20) {
+    dft_ab<5, 4, INV>(v, tw);
+  } else if constexpr (K == 24) {
+    dft_ab<3, 8, INV>(v, tw);
+  } else {
+    static_assert(K == 1, "unsupported register-FFT size");
+  }
+}
+
+// Ring lengths N = 32 K with a register FFT (K <= 24 keeps v[] at 96 registers).
+__host__ __device__ constexpr bool reg_fft_k_ok(int K) {
+  return K == 1 || K == 2 || K == 3 || K == 4 || K == 5 || K == 6 || K == 8 || K == 10 ||
+         K == 12 || K == 16 || K == 20 || K == 24;
+}
+
+// Per-lane twiddles of the cross-lane stages h = 16, 8, 4: W_{2h}^(l mod h)
+// on the upper lane of each pair, 1 on the lower one.
+template <int K, bool INV>
+__device__ __forceinline__ void cross_twiddles(double2 (&wst)[3], const double2* tw, int lane) {
+#pragma unroll
+  for (int st = 0; st < 3; ++st) {
+    const int h = 16 >> st;
+    const int j = lane & (h - 1);
+    wst[st] = (lane & h) ? tw_at(tw, j * (16 / h) * K, INV) : mk2(1.0, 0.0);
+  }
+}
+
+// Full N-point transform (see the header comment); wst from cross_twiddles.
+template <int K, bool INV>
+__device__ __forceinline__ void ring_fft(double2 (&v)[K], const double2* tw, int lane,
+                                         const double2 (&wst)[3]) {
+  dft_k<K, INV>(v, tw);
+  // W_N^(lane m1) from the gathered powers W_N^(lane 2^b) (2^b < K, so
+  // lane 2^b < N) by at most 4 products: 5 table gathers instead of K - 1
+  constexpr int NB = K > 16 ? 5 : K > 8 ? 4 : K > 4 ? 3 : K > 2 ? 2 : 1;
+  double2 wp[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) wp[b] = tw_at(tw, lane << b, INV);
+#pragma unroll
+  for (int m1 = 1; m1 < K; ++m1) {
+    double2 w = mk2(1.0, 0.0);
+    bool first = true;
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if ((m1 >> b) & 1) {
+        w = first ? wp[b] : cmul(w, wp[b]);
+        first = false;
+      }
+    v[m1] = cmul(v[m1], w);
+  }
+#pragma unroll
+  for (int st = 0; st < 5; ++st) {
+    const int h = 16 >> st;
+    const bool up = (lane & h) != 0;
+    const double sg = up ? -1.0 : 1.0;
+    const bool rot = (st == 3) && up && (lane & 1);   // h = 2: W_4^1 on odd upper lanes
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      double2 p;
+      p.x = __shfl_xor_sync(kFull, v[q].x, h);
+      p.y = __shfl_xor_sync(kFull, v[q].y, h);
+      // lower lane: own + partner; upper lane: (partner - own) * twiddle
+      double2 d = mk2(fma(sg, v[q].x, p.x), fma(sg, v[q].y, p.y));
+      if (st < 3) {
+        d = cmul(d, wst[st]);
+      } else if (st == 3) {
+        const double2 r = rot_mi(d, INV);
+        d = rot ? r : d;
+      }
+      v[q] = d;
+    }
+  }
+}
+
+// Output index held by (lane, slot m1) after ring_fft.
+template <int K>
+__device__ __forceinline__ int ring_out_index(int lane, int m1) {
+  return m1 + K * (int)(__brev((unsigned)lane) >> 27);
+}
+
+}  // namespace swfft
