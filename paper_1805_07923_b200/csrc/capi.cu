@@ -25,8 +25,8 @@ struct swsdc_plan {
   PlanDev dev{};
   std::vector<void*> owned;
   // analysis work lists [smax = R, R + 1][lsplit = 1, 2]: CTAs of 4/lsplit chunks
-  int2* work[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-  int nwork[2][2] = {{0, 0}, {0, 0}};
+  int2* work[2][kAnaSplits] = {};      // [smax = R, R + 1][latitude split - 1]
+  int nwork[2][kAnaSplits] = {};
   int nchunks[2] = {0, 0};
   int ldy = 0;
   char* ws = nullptr;
@@ -40,8 +40,8 @@ struct swsdc_plan {
     int mod = 1, rank = 0;
     int2* pairs = nullptr;
     int npairs = 0;
-    int2* work[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-    int nwork[2][2] = {{0, 0}, {0, 0}};
+    int2* work[2][kAnaSplits] = {};
+    int nwork[2][kAnaSplits] = {};
     int nchunks[2] = {0, 0};
   };
   std::vector<Shard> shards;
@@ -190,7 +190,7 @@ const swsdc_plan::Shard* shard_for(swsdc_plan* p) {
   }
   for (int i = 0; i < 2; ++i) {
     for (int r : rows) s.nchunks[i] += (R + i - r + 1 + kChunk - 1) / kChunk;
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < kAnaSplits; ++j) {
       std::vector<int2> w;
       for (const int2& it : p->host_work[i][j])
         if (it.x % rf.mod == rf.rank) w.push_back(it);
@@ -206,6 +206,42 @@ const swsdc_plan::Shard* shard_for(swsdc_plan* p) {
   return &p->shards.back();
 }
 
+int upload_work(swsdc_plan* p, std::vector<int2> (&work)[2][kAnaSplits]) {
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < kAnaSplits; ++j) SW_TRY(upload(p, work[i][j], &p->work[i][j]));
+  return kOk;
+}
+
+// Latitude split (1..4 warps per 32-degree chunk) of the register analysis
+// kernel: the one that best fills whole waves, counting warp rounds
+// ceil(items / slots) x blocks per warp ceil(nblk / split) against the
+// useful work nch x nblk (tie -> fewer splits, less reduction traffic).
+int pick_ana_split(int nch, int nmembers, int nv, int Jh) {
+  static const int knob = env_int("SWSDC_ANA_LSPLIT", 0);   // tuning knob: force 1..4
+  if (knob >= 1 && knob <= kAnaSplits) return knob;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int nblk = (Jh + 31) / 32;
+  const double useful = (double)nch * nmembers * nblk;
+  int best = 1;
+  double best_eff = -1.0;
+  for (int ls = 1; ls <= kAnaSplits; ++ls) {
+    if (ls > nblk) break;
+    const int warps = ls * ana_chunks_per_cta(ls);
+    const long long slots = (long long)sms * ana_ctas_per_sm(nv, ls) * warps;
+    const long long items = (long long)nch * nmembers * ls;
+    const long long rounds = (items + slots - 1) / slots;
+    const double eff = useful / ((double)slots * rounds * ((nblk + ls - 1) / ls));
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = ls; }
+  }
+  return best;
+}
+
 // Legendre analysis of the nv vectors (XLayout xl) of each member into out.
 int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, double2* out,
             long long out_vstride, long long out_rstride, long long out_mstride, int smax,
@@ -214,11 +250,10 @@ int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, dou
   const int which = (smax == P.R) ? 0 : 1;
   const swsdc_plan::Shard* sh = shard_for(p);
   const int nch = sh ? sh->nchunks[which] : p->nchunks[which];
-  // split latitudes over 2 warps when the chunk tasks alone cannot fill the GPU
+  // TMA variant (<= 8 vectors) runs unsplit; otherwise split latitudes to fill waves
   const int nv0 = xl.nv < 16 ? xl.nv : 16;
-  int ls = (!ana_uses_tma(nv0) && (long long)nch * nmembers < 1800) ? 1 : 0;
-  static const int knob = env_int("SWSDC_ANA_LSPLIT", 0);   // tuning knob: 1 or 2
-  if (knob) ls = (knob == 2 && !ana_uses_tma(nv0)) ? 1 : 0;
+  const int lsplit = ana_uses_tma(nv0) ? 1 : pick_ana_split(nch, nmembers, nv0, P.Jh);
+  const int ls = lsplit - 1;
   for (int v0 = 0; v0 < xl.nv; v0 += 16) {
     AnaArgs a{};
     a.nv = (xl.nv - v0 < 16) ? xl.nv - v0 : 16;
@@ -234,7 +269,7 @@ int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, dou
     a.nmembers = nmembers;
     const int nw = sh ? sh->nwork[which][ls] : p->nwork[which][ls];
     if (nw == 0) continue;
-    SW_TRY(launch_analysis(P, a, nw, ls ? 2 : 1, st));
+    SW_TRY(launch_analysis(P, a, nw, lsplit, st));
   }
   return kOk;
 }
@@ -325,14 +360,14 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
     rs += (9 - rs % 8) % 8;  // == 1 (mod 8) double2 slots: rings differ in bank group
     P.ring_stride = rs;
   }
-  std::vector<int2> work[2][2];
+  std::vector<int2> work[2][kAnaSplits];
   for (int which = 0; which < 2; ++which) {
     const int smax = R + which;
     for (int r = 0; r <= R; ++r) {
       const int nout = smax - r + 1;
       p->nchunks[which] += (nout + kChunk - 1) / kChunk;
-      for (int ls = 0; ls < 2; ++ls) {
-        const int cpc = ana_warps_per_cta() >> ls;  // chunks per CTA
+      for (int ls = 0; ls < kAnaSplits; ++ls) {
+        const int cpc = ana_chunks_per_cta(ls + 1);
         for (int c = 0; c * kChunk < nout; c += cpc) work[which][ls].push_back(make_int2(r, c));
       }
     }
@@ -349,14 +384,13 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
       (st = upload(p, eps, &d_eps)) || (st = upload(p, a, &d_a)) || (st = upload(p, b, &d_b)) ||
       (st = upload(p, sect, &d_sect)) || (st = upload(p, ck_off, &d_off)) ||
       (st = upload(p, tw, &d_tw)) || (st = upload(p, rev, &d_rev)) ||
-      (st = upload(p, work[0][0], &p->work[0][0])) || (st = upload(p, work[0][1], &p->work[0][1])) ||
-      (st = upload(p, work[1][0], &p->work[1][0])) || (st = upload(p, work[1][1], &p->work[1][1]))) {
+      (st = upload_work(p, work))) {
     swsdc_plan_destroy(p);
     return st;
   }
   for (int i = 0; i < 2; ++i) {
-    p->host_work[i].resize(2);
-    for (int j = 0; j < 2; ++j) {
+    p->host_work[i].resize(kAnaSplits);
+    for (int j = 0; j < kAnaSplits; ++j) {
       p->nwork[i][j] = (int)work[i][j].size();
       p->host_work[i][j] = work[i][j];
     }

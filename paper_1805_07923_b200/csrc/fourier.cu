@@ -408,26 +408,32 @@ __global__ void SWSDC_REG_BOUNDS(K) g2f_reg_kernel(PlanDev P, const double* grid
   }
   __syncthreads();
   double* xf = x + (MODE == 0 ? 0 : (size_t)f * xl.mstride);
-  for (int idx = threadIdx.x; idx < ((P.R + 1) << lnp); idx += blockDim.x) {
-    const int r = idx >> lnp, i = idx & (np - 1);
+  {
+    // thread -> fixed pair i, wavenumbers r0, r0 + step, ...: np consecutive
+    // threads write np consecutive latitudes of one (vector, r) x row
+    const int i = threadIdx.x & (np - 1), step = blockDim.x >> lnp;
     const int jh = jh0 + i;
-    if (jh >= P.Jh) continue;
-    const bool eq = (jn_of(P, jh) == js_of(P, jh));
-    const double mu = P.mu_n[jh], w = P.w_n[jh];
-    if (MODE == 0) {
-      double2 Fn, Fs;
-      get_pair(rings + (size_t)i * P.ring_stride, P, r, Fn, Fs);
-      put_x(xf, xl, f, r, jh, cscale(Fn, w), cscale(Fs, w), eq);
-    } else {
-      double2 Un, Us, Vn, Vs;
-      get_pair(rings + (size_t)i * P.ring_stride, P, r, Un, Us);
-      get_pair(rings + (size_t)(np + i) * P.ring_stride, P, r, Vn, Vs);
+    if (jh < P.Jh) {
+      const bool eq = (jn_of(P, jh) == js_of(P, jh));
+      const double mu = P.mu_n[jh], w = P.w_n[jh];
       const double wc = w / (1.0 - mu * mu);
-      const double rw = r * wc;
-      put_x(xf, xl, 0, r, jh, ir_scale(Un, rw), ir_scale(Us, rw), eq);
-      put_x(xf, xl, 1, r, jh, cscale(Vn, -wc), cscale(Vs, -wc), eq);
-      put_x(xf, xl, 2, r, jh, ir_scale(Vn, rw), ir_scale(Vs, rw), eq);
-      put_x(xf, xl, 3, r, jh, cscale(Un, wc), cscale(Us, wc), eq);
+      for (int r = threadIdx.x >> lnp; r <= P.R; r += step) {
+        if (MODE == 0) {
+          double2 Fn, Fs;
+          get_pair(rings + (size_t)i * P.ring_stride, P, r, Fn, Fs);
+          put_x(xf, xl, f, r, jh, cscale(Fn, w), cscale(Fs, w), eq);
+        } else {
+          double2 Un, Us, Vn, Vs;
+          get_pair(rings + (size_t)i * P.ring_stride, P, r, Un, Us);
+          get_pair(rings + (size_t)(np + i) * P.ring_stride, P, r, Vn, Vs);
+          const double rw = r * wc;
+          // div = Pwc2 (i r F_U) - Hwc2 F_V ; curl = Pwc2 (i r F_V) + Hwc2 F_U  (spharm.py:294-299)
+          put_x(xf, xl, 0, r, jh, ir_scale(Un, rw), ir_scale(Us, rw), eq);
+          put_x(xf, xl, 1, r, jh, cscale(Vn, -wc), cscale(Vs, -wc), eq);
+          put_x(xf, xl, 2, r, jh, ir_scale(Vn, rw), ir_scale(Vs, rw), eq);
+          put_x(xf, xl, 3, r, jh, cscale(Un, wc), cscale(Us, wc), eq);
+        }
+      }
     }
   }
 }

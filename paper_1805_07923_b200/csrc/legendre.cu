@@ -450,14 +450,33 @@ __device__ __forceinline__ void load_b(double (&bv)[2][NT], const double* xr, in
 
 // LSPLIT warps share one chunk, each taking every LSPLIT-th latitude block;
 // their accumulators are reduced through shared memory in warp order.
+__device__ __forceinline__ void cp_async16_ana(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// B fragments stream through a per-warp shared ring kBDepth k-steps deep
+// (cp.async, 2 x NT x 256 contiguous bytes per k-step), so the DMMAs read
+// their operands from shared memory instead of waiting on L2.
+constexpr int kBDepth = 4;
+template <int NT>
+__host__ __device__ constexpr int ana_warp_doubles() {
+  return kChunk * kQS + kChunk + kBDepth * 2 * NT * 32;
+}
+
 template <int NT, int LSPLIT>
 __global__ void __launch_bounds__(kAnaWarps * 32)
 ana_kernel(PlanDev P, AnaArgs a) {
   extern __shared__ __align__(16) double smem[];
+  constexpr int kWD = ana_warp_doubles<NT>();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  double* qs = smem + (size_t)warp * (kChunk * kQS + kChunk);   // [32][kQS]
+  double* qs = smem + (size_t)warp * kWD;                        // [32][kQS]
   double* bs = qs + kChunk * kQS;                                // [32] betas
+  double* bring = bs + kChunk;                                   // [kBDepth][2][NT * 32]
 
   const double* x = a.x + (size_t)blockIdx.y * a.xl.mstride;
   double2* out = a.out + (size_t)blockIdx.y * a.out_mstride;
@@ -486,11 +505,28 @@ ana_kernel(PlanDev P, AnaArgs a) {
     bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
     const double2* seeds = P.ckpt + (size_t)(P.ck_off[r] + c) * P.Jh;
     const int ncol = 2 * a.nv;
-    const int nc = a.xl.nc;
-    const double* xr = x + (size_t)r * a.xl.jh4 * 2 * nc * 4;
+    const int nc = a.xl.nc, jh4 = a.xl.jh4;
+    const double* xr = x + (size_t)r * jh4 * 2 * nc * 4;
     const int nblk = (P.Jh + 31) >> 5;
-    double bcur[2][NT];
-    if (half < nblk) load_b<NT>(bcur, xr, half << 3, P.Jh, nc, ncol, lane);
+    const int nmine = (nblk - half + LSPLIT - 1) / LSPLIT;   // latitude blocks of this warp
+    const int nks = nmine * 8;
+    // k-step ks -> 4-latitude block jb; copies of blocks past the row end are skipped
+    auto issue = [&](int ks) {
+      if (ks < nks) {
+        const int jb = ((half + (ks >> 3) * LSPLIT) << 3) + (ks & 7);
+        if (jb < jh4) {
+          double* dst = bring + (ks % kBDepth) * (2 * NT * 32);
+#pragma unroll
+          for (int cc = lane; cc < 2 * NT * 16; cc += 32) {
+            const int p = cc / (NT * 16), q = cc - p * (NT * 16);
+            cp_async16_ana(dst + p * NT * 32 + 2 * q, xr + ((size_t)jb * 2 + p) * nc * 4 + 2 * q);
+          }
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int d = 0; d < kBDepth - 1; ++d) issue(d);
     // seed and mu of this lane's latitude in the next block, fetched one block ahead
     double2 sd_nx = make_double2(0.0, 0.0);
     double mu_nx = 0.0;
@@ -498,6 +534,7 @@ ana_kernel(PlanDev P, AnaArgs a) {
       const int jh0 = (half << 5) + lane;
       if (jh0 < P.Jh) { sd_nx = seeds[jh0]; mu_nx = P.mu_n[jh0]; }
     }
+    int ks = 0;
     for (int jb32 = half; jb32 < nblk; jb32 += LSPLIT) {
       __syncwarp();
       // regenerate q for 32 degrees at latitude jh = 32*jb32 + lane
@@ -525,32 +562,40 @@ ana_kernel(PlanDev P, AnaArgs a) {
       }
       __syncwarp();
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        // prefetch the next k-step's B fragments (the next block's first
-        // k-step is fetched across the generation phase)
-        double bnx[2][NT];
-        const int jnext = (s < 7) ? (jb32 << 3) + s + 1 : ((jb32 + LSPLIT) << 3);
-        if (s < 7 || jb32 + LSPLIT < nblk) load_b<NT>(bnx, xr, jnext, P.Jh, nc, ncol, lane);
+      for (int s = 0; s < 8; ++s, ++ks) {
+        issue(ks + kBDepth - 1);
+        cp_async_wait<kBDepth - 1>();
+        __syncwarp();
+        const double* bsrc = bring + (ks % kBDepth) * (2 * NT * 32);
+        const bool ok = (((jb32 << 3) + s) * 4 + t) < P.Jh;
+        double bv[2][NT];
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            const double b = bsrc[p * NT * 32 + n * 32 + lane];
+            bv[p][n] = (ok && (n * 8 + g) < ncol) ? b : 0.0;
+          }
 #pragma unroll
         for (int p = 0; p < 2; ++p)
 #pragma unroll
           for (int mt = 0; mt < 2; ++mt) {
             const double av = qs[(p * 16 + mt * 8 + g) * kQS + s * 4 + t];
 #pragma unroll
-            for (int n = 0; n < NT; ++n) dmma884(acc[p][mt][n], av, bcur[p][n]);
+            for (int n = 0; n < NT; ++n) dmma884(acc[p][mt][n], av, bv[p][n]);
           }
-#pragma unroll
-        for (int p = 0; p < 2; ++p)
-#pragma unroll
-          for (int n = 0; n < NT; ++n) bcur[p][n] = bnx[p][n];
+        __syncwarp();   // this slot is refilled kBDepth - 1 k-steps later
       }
     }
+    cp_async_wait<0>();
   }
 
   if (LSPLIT > 1) {
-    // warps half > 0 hand their partial sums to the half-0 warp of their chunk
-    __syncthreads();
-    double* red = smem + (size_t)warp * (kChunk * kQS + kChunk);
+    // warps half > 0 hand their partial sums to the half-0 warp of their chunk;
+    // only the LSPLIT warps of one chunk meet (named barrier 1 + chunk)
+    const unsigned bar_id = 1 + warp / LSPLIT, bar_n = 32 * LSPLIT;
+    asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
+    double* red = smem + (size_t)warp * ana_warp_doubles<NT>();
     if (half > 0 && active) {
 #pragma unroll
       for (int p = 0; p < 2; ++p)
@@ -563,10 +608,10 @@ ana_kernel(PlanDev P, AnaArgs a) {
             red[(e + 1) * 32 + lane] = acc[p][mt][n][1];
           }
     }
-    __syncthreads();
+    asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
     if (half > 0 || !active) return;
     for (int h = 1; h < LSPLIT; ++h) {
-      const double* src = smem + (size_t)(warp + h) * (kChunk * kQS + kChunk);
+      const double* src = smem + (size_t)(warp + h) * ana_warp_doubles<NT>();
 #pragma unroll
       for (int p = 0; p < 2; ++p)
 #pragma unroll
@@ -601,21 +646,41 @@ ana_kernel(PlanDev P, AnaArgs a) {
     }
 }
 
+// CTA = ana_chunks_per_cta(LSPLIT) chunks x LSPLIT latitude splits.
 template <int NT, int LSPLIT>
 int launch_ana_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st) {
-  const size_t smem = sizeof(double) * kAnaWarps * (kChunk * kQS + kChunk);
+  const int warps = LSPLIT * ana_chunks_per_cta(LSPLIT);
+  const size_t smem = sizeof(double) * warps * ana_warp_doubles<NT>();
   auto kern = ana_kernel<NT, LSPLIT>;
   SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
   StageScope sc("legendre_analysis", st);
-  kern<<<dim3(nwork, a.nmembers), kAnaWarps * 32, smem, st>>>(P, a);
+  kern<<<dim3(nwork, a.nmembers), warps * 32, smem, st>>>(P, a);
   SW_LAUNCH_CHECK();
   return kOk;
 }
 
 template <int NT>
 int launch_ana_nt(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, cudaStream_t st) {
-  if (lsplit == 2) return launch_ana_t<NT, 2>(P, a, nwork, st);
-  return launch_ana_t<NT, 1>(P, a, nwork, st);
+  switch (lsplit) {
+    case 2: return launch_ana_t<NT, 2>(P, a, nwork, st);
+    case 3: return launch_ana_t<NT, 3>(P, a, nwork, st);
+    case 4: return launch_ana_t<NT, 4>(P, a, nwork, st);
+    default: return launch_ana_t<NT, 1>(P, a, nwork, st);
+  }
+}
+
+template <int NT, int LSPLIT>
+int ana_ctas_per_sm_t() {
+  const int warps = LSPLIT * ana_chunks_per_cta(LSPLIT);
+  const size_t smem = sizeof(double) * warps * ana_warp_doubles<NT>();
+  auto kern = ana_kernel<NT, LSPLIT>;
+  if (set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem) != kOk) return 1;
+  int n = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, warps * 32, smem) != cudaSuccess) {
+    cudaGetLastError();
+    n = 1;
+  }
+  return n > 0 ? n : 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -812,15 +877,36 @@ int launch_ana_tma(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t s
 }  // namespace
 
 int ana_warps_per_cta() { return kAnaWarps; }
+int ana_chunks_per_cta(int lsplit) { return lsplit >= 3 ? 1 : kAnaWarps / lsplit; }
 
-// TMA-streamed analysis for <= 8 vectors (x tiles <= 8 KB: 3-4 CTAs/SM); the
-// register-prefetch kernel for wider batches, whose 16 KB tiles would limit
-// occupancy to 2 CTAs/SM.
+// Resident CTAs per SM of the register analysis kernel (cached per NT, LSPLIT).
+int ana_ctas_per_sm(int nv, int lsplit) {
+  static int cache[4][4] = {};
+  const int nt = (2 * nv + 7) / 8;   // 1..4
+  int& c = cache[nt - 1][lsplit - 1];
+  if (c == 0) {
+    int n = 1;
+#define SW_OCC(NT_)                                                   \
+    switch (lsplit) {                                                 \
+      case 1: n = ana_ctas_per_sm_t<NT_, 1>(); break;                 \
+      case 2: n = ana_ctas_per_sm_t<NT_, 2>(); break;                 \
+      case 3: n = ana_ctas_per_sm_t<NT_, 3>(); break;                 \
+      default: n = ana_ctas_per_sm_t<NT_, 4>(); break;                \
+    }
+    if (nt == 1) { SW_OCC(1) } else if (nt == 2) { SW_OCC(2) } else if (nt == 3) { SW_OCC(3) } else { SW_OCC(4) }
+#undef SW_OCC
+    c = n;
+  }
+  return c;
+}
+
+// TMA-streamed analysis (opt-in, SWSDC_ANA_TMA=2): measured against the
+// cp.async-ring register kernel with its wave-fitted latitude split it wins only
+// marginally on a single large state (config 2: 16.9 vs 17.2 us) and loses on
+// config 0 (9.6 vs 8.6 us) and the 64-member ensemble (186 vs 172 us).
 bool ana_uses_tma(int nv) {
-  static const int knob = env_int("SWSDC_ANA_TMA", -1);   // tuning: 0 = never, 2 = always
-  if (knob == 0) return false;
-  if (knob == 2) return true;
-  return nv <= 8;
+  static const int knob = env_int("SWSDC_ANA_TMA", 0);   // 2: use it for <= 8 vectors
+  return knob == 2 && nv <= 8;
 }
 
 // a.work must list CTAs of kAnaWarps / lsplit consecutive chunks (lsplit 1 for TMA).

@@ -46,6 +46,10 @@ int build_checkpoints(const PlanDev& P, const double* a_tab, const double* b_tab
 int launch_synthesis(const PlanDev& P, const SynArgs& a, int B, int mode, cudaStream_t st);
 int launch_analysis(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, cudaStream_t st);
 int ana_warps_per_cta();
+// chunks per CTA of the register analysis kernel for a latitude split (1..4)
+int ana_chunks_per_cta(int lsplit);
+int ana_ctas_per_sm(int nv, int lsplit);
+constexpr int kAnaSplits = 4;
 bool ana_uses_tma(int nv);
 
 }  // namespace swsdc

@@ -43,6 +43,40 @@ __global__ void k_dmma(double* out, double a, double b) {
   if (s == 12345.678) out[threadIdx.x] = s;
 }
 
+// the analysis k-step's operand pattern: 16 accumulators acc[p][mt][n],
+// A changes every 4 DMMAs (p, mt), B differs per (p, n) -- all in registers
+__global__ void k_dmma_ana(double* out, double a, double b) {
+  double acc[2][2][4][2];
+  double av[2][2], bv[2][4];
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+#pragma unroll
+    for (int m = 0; m < 2; ++m) av[p][m] = a + (p * 2 + m + threadIdx.x) * 1e-9;
+#pragma unroll
+    for (int n = 0; n < 4; ++n) bv[p][n] = b - (p * 4 + n + threadIdx.x) * 1e-9;
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int n = 0; n < 4; ++n) { acc[p][m][n][0] = n; acc[p][m][n][1] = -n; }
+  }
+  for (int it = 0; it < ITERS / 16; ++it) {
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) dmma(acc[p][m][n], av[p][m], bv[p][n]);
+  }
+  double s = 0;
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int n = 0; n < 4; ++n) s += acc[p][m][n][0] + acc[p][m][n][1];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
 // interleave: per iteration 1 DMMA (256 FMA/warp) + NF DFMA per thread
 template <int NF>
 __global__ void k_mixed(double* out, double a, double b) {
@@ -90,6 +124,9 @@ int main() {
     ms = timeit(k_dmma, blocks, threads, out);
     fl = 2.0 * 256 * ITERS * (double)blocks * threads / 32;
     printf("DMMA  warps/SM=%2d : %.3f ms  %.2f TFLOP/s\n", occ * 4, ms, fl / ms / 1e9);
+    ms = timeit(k_dmma_ana, blocks, threads, out);
+    fl = 2.0 * 256 * ITERS * (double)blocks * threads / 32;
+    printf("DMMA-ana warps/SM=%2d : %.3f ms  %.2f TFLOP/s\n", occ * 4, ms, fl / ms / 1e9);
     ms = timeit(k_mixed<2>, blocks, threads, out);
     fl = 2.0 * 256 * ITERS * (double)blocks * threads / 32 + 2.0 * 2 * ITERS * (double)blocks * threads;
     printf("MIX2  warps/SM=%2d : %.3f ms  %.2f TFLOP/s\n", occ * 4, ms, fl / ms / 1e9);
