@@ -242,6 +242,62 @@ int pick_ana_split(int nch, int nmembers, int nv, int Jh) {
   return best;
 }
 
+// Grid workspace of the split F_E path (5 grids per state).  During stream
+// capture it cannot grow: returns false so the caller can use the fused kernel.
+int grow_grid_ws(swsdc_plan* p, size_t need, cudaStream_t st, bool* ok) {
+  *ok = true;
+  if (need <= p->grid_bytes) return kOk;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+    *ok = false;
+    return kOk;
+  }
+  if (p->grid_ws) { SW_CUDA(cudaDeviceSynchronize()); SW_CUDA(cudaFree(p->grid_ws)); }
+  p->grid_ws = nullptr;
+  p->grid_bytes = 0;
+  SW_CUDA(cudaMalloc(&p->grid_ws, need));
+  p->grid_bytes = need;
+  return kOk;
+}
+
+// F_E grid stage: fused one-pair-per-CTA kernel, or the split path (grids
+// through the workspace) for n_lon too large for the fused rings, when forced,
+// or for batches too small to fill the GPU (swe_split_preferred).
+int fe_grid_stage(swsdc_plan* p, bool nl, const double2* eo, int batch, double* x,
+                  const XLayout& xl, double omega, double radius, cudaStream_t st, int jh_begin,
+                  int jh_end) {
+  const PlanDev& P = p->dev;
+  const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
+  const bool fits = swe_grid_fits(P);
+  bool split = !fits || p->force_split ||
+               swe_split_preferred(P, (long long)(jh_end - jh_begin) * batch);
+  const long long gfield = (long long)P.I * P.J;
+  const bool reg = fourier_reg_fft(P);
+  // ring layout (register-FFT split): Jh x I complex per field; grid layout: I x J real
+  const size_t per_field = reg ? sizeof(double2) * (size_t)P.Jh * P.I : sizeof(double) * gfield;
+  if (split) {
+    bool ok = true;
+    SW_TRY(grow_grid_ws(p, per_field * 5 * batch, st, &ok));
+    if (!ok) {
+      if (!fits) {
+        set_error("grid workspace too small during stream capture");
+        return kUsage;
+      }
+      split = false;
+    }
+  }
+  if (!split)
+    return launch_swe_grid(P, nl, eo, 5 * fstride, x, xl, batch, omega, radius, st, jh_begin,
+                           jh_end);
+  if (reg)
+    return launch_swe_split_reg(P, nl, eo, fstride, reinterpret_cast<double2*>(p->grid_ws), x, xl,
+                                batch, omega, radius, st, jh_begin, jh_end);
+  double* g = reinterpret_cast<double*>(p->grid_ws);
+  SW_TRY(launch_fourier_to_grid(P, eo, fstride, g, gfield, 5 * batch, st, jh_begin, jh_end));
+  return launch_swe_products(P, nl, g, gfield, 5 * gfield, x, xl, batch, omega, radius, st,
+                             jh_begin, jh_end);
+}
+
 // Legendre analysis of the nv vectors (XLayout xl) of each member into out.
 int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, double2* out,
             long long out_vstride, long long out_rstride, long long out_mstride, int smax,
@@ -443,8 +499,10 @@ int swsdc_plan_config(swsdc_plan* p, int key, int value) {
 
 int swsdc_plan_reserve(swsdc_plan* p, int fields) {
   if (!p || fields < 0) { set_error("bad arguments"); return kUsage; }
-  if (!swe_grid_fits(p->dev) || p->force_split) {
-    const size_t need = sizeof(double) * (size_t)p->dev.I * p->dev.J * fields;
+  // fields ~ 5 per state: the split F_E path needs the grid workspace
+  if (!swe_grid_fits(p->dev) || p->force_split ||
+      swe_split_preferred(p->dev, (long long)p->dev.Jh * std::max(1, fields / 5))) {
+    const size_t need = sizeof(double2) * (size_t)p->dev.I * (p->dev.Jh + 1) * fields;
     if (need > p->grid_bytes) {
       if (p->grid_ws) { SW_CUDA(cudaDeviceSynchronize()); SW_CUDA(cudaFree(p->grid_ws)); }
       p->grid_ws = nullptr;
@@ -568,29 +626,7 @@ int swsdc_eval_fe(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, c
   a.eo_mstride = 5 * fstride;
   a.nmembers = batch;
   SW_TRY(launch_synthesis(P, a, 5, kSynSWE, S(stream)));
-  if (swe_grid_fits(P) && !p->force_split) {
-    SW_TRY(launch_swe_grid(P, nl, eo, 5 * fstride, x, xl, batch, q->omega, q->radius, S(stream)));
-  } else {
-    // large n_lon: grids through HBM (p->grid_ws), products transformed pairwise
-    const long long gfield = (long long)P.I * P.J;
-    const size_t need = sizeof(double) * (size_t)gfield * 5 * batch;
-    if (need > p->grid_bytes) {
-      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      if (cudaStreamIsCapturing(S(stream), &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
-        set_error("grid workspace too small during stream capture");
-        return kUsage;
-      }
-      if (p->grid_ws) { SW_CUDA(cudaDeviceSynchronize()); SW_CUDA(cudaFree(p->grid_ws)); }
-      p->grid_ws = nullptr;
-      p->grid_bytes = 0;
-      SW_CUDA(cudaMalloc(&p->grid_ws, need));
-      p->grid_bytes = need;
-    }
-    double* g = reinterpret_cast<double*>(p->grid_ws);
-    SW_TRY(launch_fourier_to_grid(P, eo, fstride, g, gfield, 5 * batch, S(stream)));
-    SW_TRY(launch_swe_products(P, nl, g, gfield, 5 * gfield, x, xl, batch, q->omega, q->radius,
-                               S(stream)));
-  }
+  SW_TRY(fe_grid_stage(p, nl, eo, batch, x, xl, q->omega, q->radius, S(stream), 0, P.Jh));
   const long long yv = (long long)(P.R + 1) * p->ldy;
   SW_TRY(ana_run(p, x, xl, batch, y, yv, p->ldy, nv * yv, P.R + 1, false, S(stream)));
   return launch_finalize_swe(P, y, nv * yv, p->ldy, reinterpret_cast<double2*>(out), 3 * plane, nl,
@@ -653,24 +689,8 @@ int swsdc_fe_grid(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, c
   if (batch == 0 || jh_begin == jh_end) return kOk;
   const bool nl = include_nonlinear != 0;
   const XLayout xl = make_xlayout(P.R, P.Jh, nl ? 7 : 2);
-  const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
   const double2* e = reinterpret_cast<const double2*>(eo);
-  if (swe_grid_fits(P) && !p->force_split)
-    return launch_swe_grid(P, nl, e, 5 * fstride, x, xl, batch, q->omega, q->radius, S(stream),
-                           jh_begin, jh_end);
-  const long long gfield = (long long)P.I * P.J;
-  const size_t need = sizeof(double) * (size_t)gfield * 5 * batch;
-  if (need > p->grid_bytes) {
-    if (p->grid_ws) { SW_CUDA(cudaDeviceSynchronize()); SW_CUDA(cudaFree(p->grid_ws)); }
-    p->grid_ws = nullptr;
-    p->grid_bytes = 0;
-    SW_CUDA(cudaMalloc(&p->grid_ws, need));
-    p->grid_bytes = need;
-  }
-  double* g = reinterpret_cast<double*>(p->grid_ws);
-  SW_TRY(launch_fourier_to_grid(P, e, fstride, g, gfield, 5 * batch, S(stream), jh_begin, jh_end));
-  return launch_swe_products(P, nl, g, gfield, 5 * gfield, x, xl, batch, q->omega, q->radius,
-                             S(stream), jh_begin, jh_end);
+  return fe_grid_stage(p, nl, e, batch, x, xl, q->omega, q->radius, S(stream), jh_begin, jh_end);
 }
 
 int swsdc_fe_analysis(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, const double* x,

@@ -24,6 +24,7 @@
 // both the butterflies and the cross-ring grid transposes are bank-conflict
 // free.  Pairs per CTA (np) is a power of two.
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "fourier.cuh"
@@ -90,7 +91,8 @@ __device__ __forceinline__ void pair_spectrum(double2 E, double2 O, int r, doubl
 // Loads are issued kU at a time before use so each thread keeps several
 // global reads in flight.
 __device__ __forceinline__ void fill_rings(double2* rings, const PlanDev& P, const double2* eo,
-                                           size_t fstride, int nr, int np, int lnp, int jh0) {
+                                           size_t fstride, int nr, int np, int lnp, int jh0,
+                                           bool natural = false) {
   constexpr int kU = 8;
   const int R = P.R, I = P.I, RS = P.ring_stride;
   const int nband = (nr * (R + 1)) << lnp;
@@ -122,8 +124,8 @@ __device__ __forceinline__ void fill_rings(double2* rings, const PlanDev& P, con
         double2 zp, zm;
         pair_spectrum(E[u], O[u], r, zp, zm);
         double2* ring = rings + (size_t)(q * np + i) * RS;
-        ring[P.rev[r]] = zp;
-        if (r != 0) ring[P.rev[I - r]] = zm;
+        ring[natural ? swfft::pad_idx(r) : P.rev[r]] = zp;
+        if (r != 0) ring[natural ? swfft::pad_idx(I - r) : P.rev[I - r]] = zm;
       }
     }
   }
@@ -131,7 +133,7 @@ __device__ __forceinline__ void fill_rings(double2* rings, const PlanDev& P, con
     const int i = z & (np - 1);
     const int qk = z >> lnp;
     const int q = qk / nmid, k = R + 1 + (qk - q * nmid);
-    rings[(size_t)(q * np + i) * RS + P.rev[k]] = d2(0.0, 0.0);
+    rings[(size_t)(q * np + i) * RS + (natural ? swfft::pad_idx(k) : P.rev[k])] = d2(0.0, 0.0);
   }
 }
 
@@ -291,7 +293,10 @@ __host__ __device__ inline int eo_row(int np) { return 2 * np + 1; }
 // smaller rings: up to 8 pairs (256 threads).
 #define SWSDC_REG_BOUNDS(K) __launch_bounds__((K) >= 16 ? 128 : 256, (K) >= 16 ? 3 : 2)
 
-template <int K>
+// RINGS: instead of the (n_lon, n_lat) grid, write each pair's ring (north,
+// south) contiguously: rings_out[f][jh][il] (double2), the internal layout of
+// the split F_E path whose consumer then reads whole rings coalesced.
+template <int K, bool RINGS = false>
 __global__ void SWSDC_REG_BOUNDS(K) f2g_reg_kernel(PlanDev P, const double2* eo,
                                                       long long eo_fstride, double* grid,
                                                       long long grid_fstride, int lnp,
@@ -341,7 +346,13 @@ __global__ void SWSDC_REG_BOUNDS(K) f2g_reg_kernel(PlanDev P, const double2* eo,
     double2* ring = rings + (size_t)warp * P.ring_stride;
 #pragma unroll
     for (int m1 = 0; m1 < K; ++m1) ring[swfft::pad_idx(swfft::ring_out_index<K>(lane, m1))] = v[m1];
+    if (RINGS) {
+      __syncwarp();
+      double2* dst = reinterpret_cast<double2*>(grid) + (size_t)f * grid_fstride + (size_t)jhw * P.I;
+      for (int il = lane; il < P.I; il += 32) dst[il] = ring[swfft::pad_idx(il)];
+    }
   }
+  if (RINGS) return;
   __syncthreads();
   {
     // thread -> fixed pair i, longitudes il0, il0 + step, ...: np consecutive
@@ -434,6 +445,226 @@ __global__ void SWSDC_REG_BOUNDS(K) g2f_reg_kernel(PlanDev P, const double* grid
           put_x(xf, xl, 3, r, jh, cscale(Un, wc), cscale(Us, wc), eq);
         }
       }
+    }
+  }
+}
+
+// Output stage shared by the fused SWE kernels: weighted analysis vectors of
+// the 7 (or 2) forward-transformed product rings (natural order) into x.
+template <bool NONLIN>
+__device__ __forceinline__ void swe_grid_output(const double2* rings, const PlanDev& P, double* xm,
+                                                const XLayout& xl, int jh, double w, double wc,
+                                                double ia) {
+  const int RS = P.ring_stride;
+  const bool eq = (jn_of(P, jh) == js_of(P, jh));
+  for (int r = threadIdx.x; r <= P.R; r += blockDim.x) {
+    double2 A1n, A1s, A2n, A2s;
+    get_pair(rings, P, r, A1n, A1s);
+    get_pair(rings + RS, P, r, A2n, A2s);
+    if (!NONLIN) {
+      put_x(xm, xl, 0, r, jh, cscale(A1n, w), cscale(A1s, w), eq);
+      put_x(xm, xl, 1, r, jh, cscale(A2n, w), cscale(A2s, w), eq);
+    } else {
+      double2 PUn, PUs, PVn, PVs, ZUn, ZUs, ZVn, ZVs, Kn, Ks;
+      get_pair(rings + 2 * RS, P, r, PUn, PUs);
+      get_pair(rings + 3 * RS, P, r, PVn, PVs);
+      get_pair(rings + 4 * RS, P, r, ZUn, ZUs);
+      get_pair(rings + 5 * RS, P, r, ZVn, ZVs);
+      get_pair(rings + 6 * RS, P, r, Kn, Ks);
+      const double rwa = r * wc * ia, wa = wc * ia;
+      // P-vectors: phi, zeta, delta, ke ; H-vectors: phi, zeta, delta
+      put_x(xm, xl, 0, r, jh, ir_scale(PUn, -rwa), ir_scale(PUs, -rwa), eq);
+      put_x(xm, xl, 1, r, jh, cadd2(cscale(A1n, w), ir_scale(ZUn, -rwa)),
+            cadd2(cscale(A1s, w), ir_scale(ZUs, -rwa)), eq);
+      put_x(xm, xl, 2, r, jh, cadd2(cscale(A2n, w), ir_scale(ZVn, rwa)),
+            cadd2(cscale(A2s, w), ir_scale(ZVs, rwa)), eq);
+      put_x(xm, xl, 3, r, jh, cscale(Kn, w), cscale(Ks, w), eq);
+      put_x(xm, xl, 4, r, jh, cscale(PVn, wa), cscale(PVs, wa), eq);
+      put_x(xm, xl, 5, r, jh, cscale(ZVn, wa), cscale(ZVs, wa), eq);
+      put_x(xm, xl, 6, r, jh, cscale(ZUn, wa), cscale(ZUs, wa), eq);
+    }
+  }
+}
+
+// Fused SWE grid stage with register FFTs (n_lon = 32 K), one latitude pair per
+// CTA.  Rings stay in natural order, so the pointwise products are computed in
+// place (each thread reads and rewrites its own grid points: no barrier, no
+// register staging), and warp w transforms rings w, w + nwarps, ...
+// K >= 16: 6 warps (5 inverse FFTs in one round) at <= 170 registers so two
+// CTAs share an SM; smaller rings: 8 warps.
+template <int K, bool NONLIN>
+__global__ void __launch_bounds__((K) >= 16 ? 192 : 256, 2) swe_grid_reg_kernel(PlanDev P, const double2* eo,
+                                                        long long eo_mstride, double* x,
+                                                        XLayout xl, double omega, double radius,
+                                                        int jh_begin) {
+  constexpr int NIN = NONLIN ? 5 : 4;
+  constexpr int NPROD = NONLIN ? 7 : 2;
+  extern __shared__ __align__(16) double2 rings[];  // [7 or 4][RS]
+  const int jh = jh_begin + blockIdx.x;
+  const int m = blockIdx.y;
+  const int RS = P.ring_stride;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const size_t fstride = (size_t)(P.R + 1) * P.Jh * 2;
+  fill_rings(rings, P, eo + (size_t)m * eo_mstride + (size_t)jh * 2, fstride, NIN, 1, 0, 0, true);
+  __syncthreads();
+  {
+    double2 wst[3];
+    swfft::cross_twiddles<K, true>(wst, P.tw, lane);
+    for (int q = warp; q < NIN; q += nwarp) {
+      double2* ring = rings + (size_t)q * RS;
+      double2 v[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
+      swfft::ring_fft<K, true>(v, P.tw, lane, wst);
+      __syncwarp();
+#pragma unroll
+      for (int m1 = 0; m1 < K; ++m1) ring[swfft::pad_idx(swfft::ring_out_index<K>(lane, m1))] = v[m1];
+    }
+  }
+  __syncthreads();
+  const double mu = P.mu_n[jh];
+  const double fn = 2.0 * omega * mu;         // f = 2 Omega mu (swe.py:178); south: -fn
+  const double c2o = 2.0 * omega / radius;    // swe.py:179
+  const double ic2 = 1.0 / (1.0 - mu * mu);   // swe.py:180
+  for (int il = threadIdx.x; il < P.I; il += blockDim.x) {
+    const int p = swfft::pad_idx(il);
+    const double2 U = rings[p], V = rings[RS + p], Z = rings[2 * RS + p], D = rings[3 * RS + p];
+    // swe.py:262,265 : tend_zeta grid = -f delta - (2 Omega/a) V ; tend_delta grid = f zeta - (2 Omega/a) U
+    rings[p] = d2(-fn * D.x - c2o * V.x, fn * D.y - c2o * V.y);
+    rings[RS + p] = d2(fn * Z.x - c2o * U.x, -fn * Z.y - c2o * U.y);
+    if (NONLIN) {
+      const double2 Ph = rings[(NIN - 1) * RS + p];
+      // swe.py:271-273 : Phi U, Phi V, zeta U, zeta V, KE = (U^2 + V^2) / (2 (1 - mu^2))
+      rings[2 * RS + p] = d2(Ph.x * U.x, Ph.y * U.y);
+      rings[3 * RS + p] = d2(Ph.x * V.x, Ph.y * V.y);
+      rings[4 * RS + p] = d2(Z.x * U.x, Z.y * U.y);
+      rings[5 * RS + p] = d2(Z.x * V.x, Z.y * V.y);
+      rings[6 * RS + p] = d2(0.5 * (U.x * U.x + V.x * V.x) * ic2, 0.5 * (U.y * U.y + V.y * V.y) * ic2);
+    }
+  }
+  __syncthreads();
+  {
+    double2 wst[3];
+    swfft::cross_twiddles<K, false>(wst, P.tw, lane);
+    for (int q = warp; q < NPROD; q += nwarp) {
+      double2* ring = rings + (size_t)q * RS;
+      double2 v[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
+      swfft::ring_fft<K, false>(v, P.tw, lane, wst);
+      __syncwarp();
+#pragma unroll
+      for (int m1 = 0; m1 < K; ++m1) ring[swfft::pad_idx(swfft::ring_out_index<K>(lane, m1))] = v[m1];
+    }
+  }
+  __syncthreads();
+  const double w = P.w_n[jh];
+  swe_grid_output<NONLIN>(rings, P, x + (size_t)m * xl.mstride, xl, jh, w, w * ic2, 1.0 / radius);
+}
+
+// Split SWE grid stage, second kernel (register FFTs): the 5 grids come from
+// HBM/L2 (written by f2g_reg_kernel); CTA (pair, member, role) stages the grid
+// rows it needs with async copies, each warp forms one product ring in
+// registers and transforms it, and the CTA writes the analysis vectors of its
+// role.  Role 0: A1, ZU, A2, ZV -> vectors 1, 2, 5, 6 (linear: A1, A2 -> 0, 1);
+// role 1: PU, PV, KE -> vectors 0, 4, 3.  Twice the CTAs of the fused kernel
+// and no inverse FFTs: for batches too small to fill the GPU one pair per CTA.
+template <int K, bool NONLIN>
+__global__ void __launch_bounds__(128) swe_fwd_reg_kernel(PlanDev P, const double2* gr,
+                                                          long long gfield, long long gmember,
+                                                          double* x, XLayout xl, double omega,
+                                                          double radius, int jh_begin) {
+  extern __shared__ __align__(16) double2 rings[];  // [4][RS] product spectra
+  const int jh = jh_begin + blockIdx.x, m = blockIdx.y, role = blockIdx.z;
+  const int RS = P.ring_stride;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int jn = jn_of(P, jh), js = js_of(P, jh);
+  // this pair's ring of field q (U/a, V/a, zeta, delta, phi'): I contiguous (north, south);
+  // the role's fields are staged whole (coalesced 16-byte async copies, all in
+  // flight at once): role 0 -> U, V, zeta, delta ; role 1 -> U, V, phi'
+  const double2* gp = gr + (size_t)m * gmember + (size_t)jh * P.I;
+  const int nst = role == 0 ? 4 : 3;
+  for (int idx = threadIdx.x; idx < nst * P.I; idx += blockDim.x) {
+    const int sidx = idx / P.I, il = idx - sidx * P.I;
+    const int q = (role == 1 && sidx == 2) ? 4 : sidx;
+    cp_async16(rings + idx, gp + (size_t)q * gfield + il);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const double2* stg = rings;   // [nst][I], unpadded
+  const double mu = P.mu_n[jh];
+  const double fn = 2.0 * omega * mu;         // f = 2 Omega mu (swe.py:178); south: -fn
+  const double c2o = 2.0 * omega / radius;    // swe.py:179
+  const double ic2 = 1.0 / (1.0 - mu * mu);   // swe.py:180
+  const int nprod = role == 0 ? (NONLIN ? 4 : 2) : 3;
+  double2 v[K];
+  const bool busy = warp < nprod;
+  if (busy) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int il = 32 * k + lane;
+      const double2 U = stg[il], V = stg[P.I + il];
+      double2 z;
+      if (role == 0) {
+        const double2 Z = stg[2 * P.I + il], D = stg[3 * P.I + il];
+        // swe.py:262,265,273 : A1 = -f delta - c2o V ; ZU = zeta U ; A2 = f zeta - c2o U ; ZV = zeta V
+        const int w = NONLIN ? warp : 2 * warp;   // linear: A1, A2 only
+        if (w == 0) z = d2(-fn * D.x - c2o * V.x, fn * D.y - c2o * V.y);
+        else if (w == 1) z = d2(Z.x * U.x, Z.y * U.y);
+        else if (w == 2) z = d2(fn * Z.x - c2o * U.x, -fn * Z.y - c2o * U.y);
+        else z = d2(Z.x * V.x, Z.y * V.y);
+      } else {
+        const double2 Ph = stg[2 * P.I + il];
+        // swe.py:271-272 : Phi U, Phi V, KE = (U^2 + V^2) / (2 (1 - mu^2))
+        if (warp == 0) z = d2(Ph.x * U.x, Ph.y * U.y);
+        else if (warp == 1) z = d2(Ph.x * V.x, Ph.y * V.y);
+        else z = d2(0.5 * (U.x * U.x + V.x * V.x) * ic2, 0.5 * (U.y * U.y + V.y * V.y) * ic2);
+      }
+      v[k] = z;
+    }
+    double2 wst[3];
+    swfft::cross_twiddles<K, false>(wst, P.tw, lane);
+    swfft::ring_fft<K, false>(v, P.tw, lane, wst);
+  }
+  __syncthreads();   // staging consumed; the product rings reuse it
+  if (busy) {
+    double2* ring = rings + (size_t)warp * RS;
+#pragma unroll
+    for (int m1 = 0; m1 < K; ++m1) ring[swfft::pad_idx(swfft::ring_out_index<K>(lane, m1))] = v[m1];
+  }
+  __syncthreads();
+  const bool eq = (jn == js);
+  const double w = P.w_n[jh], wc = w * ic2, ia = 1.0 / radius;
+  const double rwa_base = wc * ia, wa = wc * ia;
+  double* xm = x + (size_t)m * xl.mstride;
+  for (int r = threadIdx.x; r <= P.R; r += blockDim.x) {
+    const double rwa = r * rwa_base;
+    if (role == 0 && !NONLIN) {
+      double2 A1n, A1s, A2n, A2s;
+      get_pair(rings, P, r, A1n, A1s);
+      get_pair(rings + RS, P, r, A2n, A2s);
+      put_x(xm, xl, 0, r, jh, cscale(A1n, w), cscale(A1s, w), eq);
+      put_x(xm, xl, 1, r, jh, cscale(A2n, w), cscale(A2s, w), eq);
+    } else if (role == 0) {
+      double2 A1n, A1s, ZUn, ZUs, A2n, A2s, ZVn, ZVs;
+      get_pair(rings, P, r, A1n, A1s);
+      get_pair(rings + RS, P, r, ZUn, ZUs);
+      get_pair(rings + 2 * RS, P, r, A2n, A2s);
+      get_pair(rings + 3 * RS, P, r, ZVn, ZVs);
+      put_x(xm, xl, 1, r, jh, cadd2(cscale(A1n, w), ir_scale(ZUn, -rwa)),
+            cadd2(cscale(A1s, w), ir_scale(ZUs, -rwa)), eq);
+      put_x(xm, xl, 2, r, jh, cadd2(cscale(A2n, w), ir_scale(ZVn, rwa)),
+            cadd2(cscale(A2s, w), ir_scale(ZVs, rwa)), eq);
+      put_x(xm, xl, 5, r, jh, cscale(ZVn, wa), cscale(ZVs, wa), eq);
+      put_x(xm, xl, 6, r, jh, cscale(ZUn, wa), cscale(ZUs, wa), eq);
+    } else {
+      double2 PUn, PUs, PVn, PVs, Kn, Ks;
+      get_pair(rings, P, r, PUn, PUs);
+      get_pair(rings + RS, P, r, PVn, PVs);
+      get_pair(rings + 2 * RS, P, r, Kn, Ks);
+      put_x(xm, xl, 0, r, jh, ir_scale(PUn, -rwa), ir_scale(PUs, -rwa), eq);
+      put_x(xm, xl, 3, r, jh, cscale(Kn, w), cscale(Ks, w), eq);
+      put_x(xm, xl, 4, r, jh, cscale(PVn, wa), cscale(PVs, wa), eq);
     }
   }
 }
@@ -748,6 +979,37 @@ int swe_launch(const PlanDev& P, const double2* eo, long long eo_mstride, double
   return kOk;
 }
 
+template <int K, bool NONLIN>
+int swe_reg_launch(const PlanDev& P, const double2* eo, long long eo_mstride, double* x,
+                   const XLayout& xl, int nmembers, double omega, double radius, int jh_begin,
+                   int jh_end, cudaStream_t st) {
+  const int nr = NONLIN ? 7 : 4;
+  const size_t smem = sizeof(double2) * nr * P.ring_stride;
+  dim3 gridDim(jh_end - jh_begin, nmembers);
+  if (gridDim.x == 0) return kOk;
+  SW_TRY(set_smem((const void*)swe_grid_reg_kernel<K, NONLIN>, smem));
+  StageScope sc("swe_grid", st);
+  swe_grid_reg_kernel<K, NONLIN><<<gridDim, K >= 16 ? 192 : 256, smem, st>>>(
+      P, eo, eo_mstride, x, xl, omega, radius, jh_begin);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+template <int K, bool NONLIN>
+int swe_fwd_reg_launch(const PlanDev& P, const double2* grids, long long gfield, long long gmember,
+                       double* x, const XLayout& xl, int nmembers, double omega, double radius,
+                       int jh_begin, int jh_end, cudaStream_t st) {
+  const size_t smem = sizeof(double2) * 4 * P.ring_stride;
+  SW_TRY(set_smem((const void*)swe_fwd_reg_kernel<K, NONLIN>, smem));
+  dim3 gridDim(jh_end - jh_begin, nmembers, NONLIN ? 2 : 1);
+  if (gridDim.x == 0) return kOk;
+  StageScope sc("swe_products", st);
+  swe_fwd_reg_kernel<K, NONLIN><<<gridDim, 128, smem, st>>>(P, grids, gfield, gmember, x, xl,
+                                                            omega, radius, jh_begin);
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
 template <bool NONLIN, bool BIGP>
 int swe_prod_launch(const PlanDev& P, const double* grids, long long gfield, long long gmember,
                     double* x, const XLayout& xl, int nmembers, double omega, double radius,
@@ -765,8 +1027,72 @@ int swe_prod_launch(const PlanDev& P, const double* grids, long long gfield, lon
 
 }  // namespace
 
+// Split F_E path with register FFTs: E/O -> 5 rings per pair (ring layout,
+// rings[m][q][jh][il]) -> products, forward FFTs, analysis vectors.
+int launch_swe_split_reg(const PlanDev& P, bool nonlinear, const double2* eo, long long eo_fstride,
+                         double2* ring_ws, double* x, const XLayout& xl, int nmembers,
+                         double omega, double radius, cudaStream_t st, int jh_begin, int jh_end) {
+  const long long gfield = (long long)P.Jh * P.I;   // double2 per field ring block
+  const int lnp = pairs_log2(P, 1), np = 1 << lnp;
+  dim3 g1((jh_end - jh_begin + np - 1) / np, 5 * nmembers);
+  const size_t smem1 = sizeof(double2) * std::max((size_t)np * P.ring_stride,
+                                                  (size_t)(P.R + 1) * eo_row(np));
+  int st1 = kOk;
+  auto first = [&](auto kk) -> int {
+    constexpr int KK = decltype(kk)::value;
+    SW_TRY(set_smem((const void*)f2g_reg_kernel<KK, true>, smem1));
+    StageScope sc("fourier_to_grid", st);
+    f2g_reg_kernel<KK, true><<<g1, 32 * np, smem1, st>>>(
+        P, eo, eo_fstride, reinterpret_cast<double*>(ring_ws), gfield, lnp, jh_begin, jh_end);
+    SW_LAUNCH_CHECK();
+    if (nonlinear)
+      return swe_fwd_reg_launch<KK, true>(P, ring_ws, gfield, 5 * gfield, x, xl, nmembers, omega,
+                                          radius, jh_begin, jh_end, st);
+    return swe_fwd_reg_launch<KK, false>(P, ring_ws, gfield, 5 * gfield, x, xl, nmembers, omega,
+                                         radius, jh_begin, jh_end, st);
+  };
+  if (g1.x == 0) return kOk;
+  switch (P.I / 32) {
+    case 1: st1 = first(std::integral_constant<int, 1>()); break;
+    case 2: st1 = first(std::integral_constant<int, 2>()); break;
+    case 3: st1 = first(std::integral_constant<int, 3>()); break;
+    case 4: st1 = first(std::integral_constant<int, 4>()); break;
+    case 5: st1 = first(std::integral_constant<int, 5>()); break;
+    case 6: st1 = first(std::integral_constant<int, 6>()); break;
+    case 8: st1 = first(std::integral_constant<int, 8>()); break;
+    case 10: st1 = first(std::integral_constant<int, 10>()); break;
+    case 12: st1 = first(std::integral_constant<int, 12>()); break;
+    case 16: st1 = first(std::integral_constant<int, 16>()); break;
+    case 20: st1 = first(std::integral_constant<int, 20>()); break;
+    case 24: st1 = first(std::integral_constant<int, 24>()); break;
+    default: set_error("register FFT size not supported"); return kUsage;
+  }
+  return st1;
+}
+
+bool fourier_reg_fft(const PlanDev& P) { return use_reg_fft(P); }
+
 bool swe_grid_fits(const PlanDev& P) {
   return sizeof(double2) * 7 * (size_t)P.ring_stride <= 160 * 1024;
+}
+
+// Small batches (few latitude pairs x members) leave the one-pair-per-CTA fused
+// kernel short of CTAs; the split path (f2g of the 5 grids, then the role-split
+// forward kernel) runs ~3x more warps.  SWSDC_SWE_SPLIT: 0 never, 2 always.
+bool swe_split_preferred(const PlanDev& P, long long pair_members) {
+  static const int knob = env_int("SWSDC_SWE_SPLIT", 1);
+  if (knob == 0 || !use_reg_fft(P)) return false;
+  if (knob == 2) return true;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  // measured (config 0 / 2): the split path wins only when the fused kernel
+  // would run well under one CTA per SM
+  return 2 * pair_members <= sms;
 }
 
 int launch_swe_products(const PlanDev& P, bool nonlinear, const double* grids, long long gfield,
@@ -818,6 +1144,15 @@ int launch_swe_grid(const PlanDev& P, bool nonlinear, const double2* eo, long lo
                     double* x, const XLayout& xl, int nmembers, double omega, double radius,
                     cudaStream_t st, int jh_begin, int jh_end) {
   if (jh_end < 0) jh_end = P.Jh;
+  if (use_reg_fft(P)) {
+    if (nonlinear) {
+      SWSDC_REG_K_SWITCH(P.I / 32, (swe_reg_launch<KK, true>(P, eo, eo_mstride, x, xl, nmembers,
+                                                             omega, radius, jh_begin, jh_end, st)));
+    } else {
+      SWSDC_REG_K_SWITCH(P.I / 32, (swe_reg_launch<KK, false>(P, eo, eo_mstride, x, xl, nmembers,
+                                                              omega, radius, jh_begin, jh_end, st)));
+    }
+  }
   const bool big = swfft::fft_needs_bigp(P.I);
   if (nonlinear) {
     if (big) return swe_launch<true, true>(P, eo, eo_mstride, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);

@@ -20,6 +20,11 @@ int launch_swe_grid(const PlanDev& P, bool nonlinear, const double2* eo, long lo
 
 // true when the fused grid kernel's 7 rings fit in shared memory
 bool swe_grid_fits(const PlanDev& P);
+bool swe_split_preferred(const PlanDev& P, long long pair_members);
+bool fourier_reg_fft(const PlanDev& P);
+int launch_swe_split_reg(const PlanDev& P, bool nonlinear, const double2* eo, long long eo_fstride,
+                         double2* ring_ws, double* x, const XLayout& xl, int nmembers,
+                         double omega, double radius, cudaStream_t st, int jh_begin, int jh_end);
 // large-n_lon path: products + forward FFTs from 5 grids in HBM
 // (grids[m * gmember + q * gfield + il * J + j], q = U/a, V/a, zeta, delta, phi')
 int launch_swe_products(const PlanDev& P, bool nonlinear, const double* grids, long long gfield,

@@ -109,3 +109,31 @@ def test_pinned_host_upload_and_download(golden):
         spharm.upload_coeffs(torch.from_numpy(c))          # pageable: refused
     with pytest.raises(ValueError):
         plan.analyze(g_ref, out=torch.empty(c.shape, dtype=torch.complex128))
+
+
+def test_tma_and_forced_split_variants_match_reference(tmp_path):
+    """The opt-in TMA analysis (SWSDC_ANA_TMA=2) and every forced latitude split
+    (SWSDC_ANA_LSPLIT=1..4) give the reference's analysis; the knobs are read once
+    per process, so each variant runs in a subprocess."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "from conftest import GOLDEN, rel_err;"
+        "from paper_1805_07923_b200 import spharm;"
+        "g = np.load(GOLDEN + '/transforms.npz');"
+        "worst = 0.0\n"
+        "for R, I, J in [(31, 96, 48), (63, 192, 96), (31, 96, 47)]:\n"
+        "    t = f'R{R}_I{I}_J{J}'\n"
+        "    plan = spharm.TransformPlan(spharm.build_gaussian_grid(J, I), R)\n"
+        "    for nb in (1, 7, 16):\n"
+        "        f = np.stack([g[t + '_g']] * nb)\n"
+        "        worst = max(worst, rel_err(plan.analyze(f)[0], g[t + '_ana']))\n"
+        "print(worst)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for env in ({"SWSDC_ANA_TMA": "2"}, {"SWSDC_ANA_LSPLIT": "1"}, {"SWSDC_ANA_LSPLIT": "2"},
+                {"SWSDC_ANA_LSPLIT": "3"}, {"SWSDC_ANA_LSPLIT": "4"}):
+        out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True,
+                             text=True, env={**os.environ, **env}, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        assert float(out.stdout.strip().splitlines()[-1]) < TOL, (env, out.stdout)
