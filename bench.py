@@ -387,17 +387,26 @@ def run_ours(args, world, rank, local):
             hbm_peak = json.load(f).get("hbm_gbs")
     except Exception:
         pass
+    # DRAM bytes per launch of the dominant kernel from the committed ncu --set full
+    # capture (profiles/r01/traffic.json), for comparison with the algorithmic bytes
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        pass
     if dom.startswith("legendre"):
         achieved = per_launch_flops[dom] / (dom_ms * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
-                "frac": achieved / peak_fp64, "traffic": None, "kernel": dom,
+                "frac": achieved / peak_fp64, "traffic": traffic, "kernel": dom,
+                "algorithmic_bytes": per_launch_bytes.get(dom),
                 "peak_kind": "fp64 FMA pipe (DFMA == DMMA on sm_100a)", "peak_source": peak_src,
                 "work": f"{NF} fields x 2*T*J flops, T=(R+1)(R+2)/2"}
     else:
         hb = hbm_peak or 6547.2
         achieved = per_launch_bytes[dom] / (dom_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hb, "unit": "GB/s",
-                "frac": achieved / hb, "traffic": None, "kernel": dom,
+                "frac": achieved / hb, "traffic": traffic, "kernel": dom,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
     pair_flops = NF * 2 * (legendre_flops(R, J) + fft_flops(I, J))
     step_s = t_ms * 1e-3 / args.steps
