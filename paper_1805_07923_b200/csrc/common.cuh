@@ -49,6 +49,39 @@ int set_max_dyn_smem(const void* kern, size_t smem);
 // in a function-local static so the environment is read once per process.
 int env_int(const char* name, int dflt);
 
+// Programmatic dependent launch (PDL).  Library kernels are launched with
+// launch_pdl, which lets a kernel's CTAs be scheduled while its stream
+// predecessor drains; every kernel begins with pdl_wait() (returns once the
+// predecessor grid has completed and its writes are visible; a no-op without
+// PDL) followed by pdl_trigger() (lets our own dependents launch as soon as all
+// our CTAs are resident).  SWSDC_PDL=0 disables the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// Explicit early trigger (SWSDC_PDL_EARLY builds): measured to cost config 2
+// ~7% (dependents land unevenly during the predecessor's tail), so by default
+// dependents launch as the predecessor's CTAs exit.
+__device__ __forceinline__ void pdl_trigger() {
+#ifdef SWSDC_PDL_EARLY
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
+}
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // RAII bracket of one kernel launch: counts it and, when profiling is on,
 // records CUDA events around it on `st` (profile.cu).
 class StageScope {

@@ -172,6 +172,8 @@ __device__ __forceinline__ void put_x(double* x, const XLayout& L, int v, int r,
 template <bool BIGP>
 __global__ void __launch_bounds__(256, 2) f2g_kernel(PlanDev P, const double2* eo, long long eo_fstride, double* grid,
                            long long grid_fstride, int lnp, int jh_begin, int jh_end) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) double2 rings[];
   const int np = 1 << lnp;
   const int f = blockIdx.y;
@@ -201,6 +203,8 @@ __global__ void __launch_bounds__(256, 2) f2g_kernel(PlanDev P, const double2* e
 template <int MODE, bool BIGP>
 __global__ void __launch_bounds__(256, 2) g2f_kernel(PlanDev P, const double* grid, const double* grid2,
                            long long grid_fstride, double* x, XLayout xl, int lnp) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NIN = (MODE == 0) ? 1 : 2;
   extern __shared__ __align__(16) double2 rings[];  // [NIN][np][RS]
   const int np = 1 << lnp;
@@ -301,6 +305,8 @@ __global__ void SWSDC_REG_BOUNDS(K) f2g_reg_kernel(PlanDev P, const double2* eo,
                                                       long long eo_fstride, double* grid,
                                                       long long grid_fstride, int lnp,
                                                       int jh_begin, int jh_end) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) double2 rings[];
   const int np = 1 << lnp;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -378,6 +384,8 @@ template <int K, int MODE>
 __global__ void SWSDC_REG_BOUNDS(K) g2f_reg_kernel(PlanDev P, const double* grid,
                                                       const double* grid2, long long grid_fstride,
                                                       double* x, XLayout xl, int lnp) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NIN = (MODE == 0) ? 1 : 2;
   extern __shared__ __align__(16) double2 rings[];  // [NIN][np][RS], natural order
   const int np = 1 << lnp;
@@ -497,6 +505,8 @@ __global__ void __launch_bounds__((K) >= 16 ? 192 : 256, 2) swe_grid_reg_kernel(
                                                         long long eo_mstride, double* x,
                                                         XLayout xl, double omega, double radius,
                                                         int jh_begin) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NIN = NONLIN ? 5 : 4;
   constexpr int NPROD = NONLIN ? 7 : 2;
   extern __shared__ __align__(16) double2 rings[];  // [7 or 4][RS]
@@ -574,6 +584,8 @@ __global__ void __launch_bounds__(128) swe_fwd_reg_kernel(PlanDev P, const doubl
                                                           long long gfield, long long gmember,
                                                           double* x, XLayout xl, double omega,
                                                           double radius, int jh_begin) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) double2 rings[];  // [4][RS] product spectra
   const int jh = jh_begin + blockIdx.x, m = blockIdx.y, role = blockIdx.z;
   const int RS = P.ring_stride;
@@ -677,6 +689,8 @@ __global__ void __launch_bounds__(128) swe_fwd_reg_kernel(PlanDev P, const doubl
 template <bool NONLIN, bool BIGP>
 __global__ void __launch_bounds__(256, 2) swe_grid_kernel(PlanDev P, const double2* eo, long long eo_mstride, double* x,
                                 XLayout xl, double omega, double radius, int jh_begin) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NIN = NONLIN ? 5 : 4;
   constexpr int NPROD = NONLIN ? 7 : 2;
   extern __shared__ __align__(16) double2 rings[];  // [7 or 4][RS]
@@ -772,6 +786,8 @@ __global__ void __launch_bounds__(256, 1) swe_prod_kernel(PlanDev P, const doubl
                                                           long long gfield, long long gmember,
                                                           double* x, XLayout xl, double omega,
                                                           double radius, int jh_begin) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) double2 rings[];  // [2][RS]
   const int jh = jh_begin + blockIdx.x, m = blockIdx.y;
   const int RS = P.ring_stride, I = P.I;
@@ -890,8 +906,7 @@ int f2g_reg_launch(const PlanDev& P, const double2* eo, long long eo_fstride, do
   dim3 gridDim((jh_end - jh_begin + np - 1) / np, nf);
   if (gridDim.x == 0) return kOk;
   StageScope sc("fourier_to_grid", st);
-  f2g_reg_kernel<K><<<gridDim, 32 * np, smem, st>>>(P, eo, eo_fstride, grid, grid_fstride, lnp,
-                                                   jh_begin, jh_end);
+  SW_CUDA(launch_pdl(f2g_reg_kernel<K>, dim3(gridDim), dim3(32 * np), smem, st, P, eo, eo_fstride, grid, grid_fstride, lnp, jh_begin, jh_end));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -905,8 +920,7 @@ int g2f_reg_launch(const PlanDev& P, const double* grid, const double* grid2,
   dim3 gridDim((P.Jh + np - 1) / np, nf);
   SW_TRY(set_smem((const void*)g2f_reg_kernel<K, MODE>, smem));
   StageScope sc(MODE == 0 ? "grid_to_fourier" : "grid_to_fourier_divcurl", st);
-  g2f_reg_kernel<K, MODE><<<gridDim, 32 * nin * np, smem, st>>>(P, grid, grid2, grid_fstride, x,
-                                                               xl, lnp);
+  SW_CUDA(launch_pdl(g2f_reg_kernel<K, MODE>, dim3(gridDim), dim3(32 * nin * np), smem, st, P, grid, grid2, grid_fstride, x, xl, lnp));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -936,8 +950,7 @@ int f2g_launch(const PlanDev& P, const double2* eo, long long eo_fstride, double
   dim3 gridDim((jh_end - jh_begin + np - 1) / np, nf);
   if (gridDim.x == 0) return kOk;
   StageScope sc("fourier_to_grid", st);
-  f2g_kernel<BIGP><<<gridDim, pick_threads(np * max_butterflies(P), BIGP), smem, st>>>(
-      P, eo, eo_fstride, grid, grid_fstride, lnp, jh_begin, jh_end);
+  SW_CUDA(launch_pdl(f2g_kernel<BIGP>, dim3(gridDim), dim3(pick_threads(np * max_butterflies(P), BIGP)), smem, st, P, eo, eo_fstride, grid, grid_fstride, lnp, jh_begin, jh_end));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -951,8 +964,7 @@ int g2f_launch(const PlanDev& P, const double* grid, const double* grid2, long l
   dim3 gridDim((P.Jh + np - 1) / np, nf);
   SW_TRY(set_smem((const void*)g2f_kernel<MODE, BIGP>, smem));
   StageScope sc(MODE == 0 ? "grid_to_fourier" : "grid_to_fourier_divcurl", st);
-  g2f_kernel<MODE, BIGP><<<gridDim, pick_threads(nin * np * max_butterflies(P), BIGP), smem, st>>>(
-      P, grid, grid2, grid_fstride, x, xl, lnp);
+  SW_CUDA(launch_pdl(g2f_kernel<MODE, BIGP>, dim3(gridDim), dim3(pick_threads(nin * np * max_butterflies(P), BIGP)), smem, st, P, grid, grid2, grid_fstride, x, xl, lnp));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -973,8 +985,7 @@ int swe_launch(const PlanDev& P, const double2* eo, long long eo_mstride, double
     return kUsage;
   }
   StageScope sc("swe_grid", st);
-  swe_grid_kernel<NONLIN, BIGP><<<gridDim, threads, smem, st>>>(
-      P, eo, eo_mstride, x, xl, omega, radius, jh_begin);
+  SW_CUDA(launch_pdl(swe_grid_kernel<NONLIN, BIGP>, dim3(gridDim), dim3(threads), smem, st, P, eo, eo_mstride, x, xl, omega, radius, jh_begin));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -989,8 +1000,7 @@ int swe_reg_launch(const PlanDev& P, const double2* eo, long long eo_mstride, do
   if (gridDim.x == 0) return kOk;
   SW_TRY(set_smem((const void*)swe_grid_reg_kernel<K, NONLIN>, smem));
   StageScope sc("swe_grid", st);
-  swe_grid_reg_kernel<K, NONLIN><<<gridDim, K >= 16 ? 192 : 256, smem, st>>>(
-      P, eo, eo_mstride, x, xl, omega, radius, jh_begin);
+  SW_CUDA(launch_pdl(swe_grid_reg_kernel<K, NONLIN>, dim3(gridDim), dim3(K >= 16 ? 192 : 256), smem, st, P, eo, eo_mstride, x, xl, omega, radius, jh_begin));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -1004,8 +1014,7 @@ int swe_fwd_reg_launch(const PlanDev& P, const double2* grids, long long gfield,
   dim3 gridDim(jh_end - jh_begin, nmembers, NONLIN ? 2 : 1);
   if (gridDim.x == 0) return kOk;
   StageScope sc("swe_products", st);
-  swe_fwd_reg_kernel<K, NONLIN><<<gridDim, 128, smem, st>>>(P, grids, gfield, gmember, x, xl,
-                                                            omega, radius, jh_begin);
+  SW_CUDA(launch_pdl(swe_fwd_reg_kernel<K, NONLIN>, dim3(gridDim), dim3(128), smem, st, P, grids, gfield, gmember, x, xl, omega, radius, jh_begin));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -1019,8 +1028,7 @@ int swe_prod_launch(const PlanDev& P, const double* grids, long long gfield, lon
   dim3 gridDim(jh_end - jh_begin, nmembers);
   if (gridDim.x == 0) return kOk;
   StageScope sc("swe_products", st);
-  swe_prod_kernel<NONLIN, BIGP><<<gridDim, BIGP ? 128 : 256, smem, st>>>(
-      P, grids, gfield, gmember, x, xl, omega, radius, jh_begin);
+  SW_CUDA(launch_pdl(swe_prod_kernel<NONLIN, BIGP>, dim3(gridDim), dim3(BIGP ? 128 : 256), smem, st, P, grids, gfield, gmember, x, xl, omega, radius, jh_begin));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -1042,8 +1050,7 @@ int launch_swe_split_reg(const PlanDev& P, bool nonlinear, const double2* eo, lo
     constexpr int KK = decltype(kk)::value;
     SW_TRY(set_smem((const void*)f2g_reg_kernel<KK, true>, smem1));
     StageScope sc("fourier_to_grid", st);
-    f2g_reg_kernel<KK, true><<<g1, 32 * np, smem1, st>>>(
-        P, eo, eo_fstride, reinterpret_cast<double*>(ring_ws), gfield, lnp, jh_begin, jh_end);
+    SW_CUDA(launch_pdl(f2g_reg_kernel<KK, true>, dim3(g1), dim3(32 * np), smem1, st, P, eo, eo_fstride, reinterpret_cast<double*>(ring_ws), gfield, lnp, jh_begin, jh_end));
     SW_LAUNCH_CHECK();
     if (nonlinear)
       return swe_fwd_reg_launch<KK, true>(P, ring_ws, gfield, 5 * gfield, x, xl, nmembers, omega,

@@ -37,6 +37,8 @@ namespace swsdc {
 // ---------------------------------------------------------------------------
 __global__ void build_checkpoints_kernel(PlanDev P, const double* a_tab, const double* b_tab,
                                          const double* sect_fac, double2* ckpt) {
+  pdl_wait();
+  pdl_trigger();
   const int jh = blockIdx.x * blockDim.x + threadIdx.x;
   if (jh >= P.Jh) return;
   const double mu = P.mu_n[jh];
@@ -68,8 +70,7 @@ int build_checkpoints(const PlanDev& P, const double* a_tab, const double* b_tab
                       const double* sect_fac, double2* ckpt, cudaStream_t st) {
   const int threads = 64;
   StageScope sc("build_checkpoints", st);
-  build_checkpoints_kernel<<<(P.Jh + threads - 1) / threads, threads, 0, st>>>(P, a_tab, b_tab,
-                                                                               sect_fac, ckpt);
+  SW_CUDA(launch_pdl(build_checkpoints_kernel, dim3((P.Jh + threads - 1) / threads), dim3(threads), 0, st, P, a_tab, b_tab, sect_fac, ckpt));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -222,6 +223,8 @@ __device__ __forceinline__ void flush_row(double2 (&E)[B][kSynNL], double2 (&O)[
 template <int B, int MODE, int NSPLIT>
 __global__ void __launch_bounds__(NSPLIT * 32)
 syn_kernel(PlanDev P, SynArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double2* cs = reinterpret_cast<double2*>(smem) + (size_t)warp * B * kCS;        // [B][kCS]
@@ -371,7 +374,7 @@ int launch_syn_t(const PlanDev& P, const SynArgs& a, cudaStream_t st) {
   auto kern = syn_kernel<B, MODE, NSPLIT>;
   SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
   StageScope sc("legendre_synthesis", st);
-  kern<<<dim3(npairs, nlg, a.nmembers), NSPLIT * 32, smem, st>>>(P, a);
+  SW_CUDA(launch_pdl(kern, dim3(dim3(npairs, nlg, a.nmembers)), dim3(NSPLIT * 32), smem, st, P, a));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -470,6 +473,8 @@ __host__ __device__ constexpr int ana_warp_doubles() {
 template <int NT, int LSPLIT>
 __global__ void __launch_bounds__(kAnaWarps * 32)
 ana_kernel(PlanDev P, AnaArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) double smem[];
   constexpr int kWD = ana_warp_doubles<NT>();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -654,7 +659,7 @@ int launch_ana_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st)
   auto kern = ana_kernel<NT, LSPLIT>;
   SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
   StageScope sc("legendre_analysis", st);
-  kern<<<dim3(nwork, a.nmembers), warps * 32, smem, st>>>(P, a);
+  SW_CUDA(launch_pdl(kern, dim3(dim3(nwork, a.nmembers)), dim3(warps * 32), smem, st, P, a));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -731,6 +736,8 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 template <int NT>
 __global__ void __launch_bounds__(kAnaWarps * 32)
 ana_tma_kernel(PlanDev P, AnaArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(128) double smem[];
   const int nc = a.xl.nc;                        // layout columns (>= 8 NT)
   const int blk_doubles = 8 * 2 * nc * 4;        // one 32-latitude tile
@@ -869,7 +876,7 @@ int launch_ana_tma(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t s
   auto kern = ana_tma_kernel<NT>;
   SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
   StageScope sc("legendre_analysis", st);
-  kern<<<dim3(nwork, a.nmembers), kAnaWarps * 32, smem, st>>>(P, a);
+  SW_CUDA(launch_pdl(kern, dim3(dim3(nwork, a.nmembers)), dim3(kAnaWarps * 32), smem, st, P, a));
   SW_LAUNCH_CHECK();
   return kOk;
 }

@@ -41,6 +41,11 @@ cudaEvent_t take_event() {
 
 }  // namespace
 
+bool pdl_enabled() {
+  static const bool on = env_int("SWSDC_PDL", 1) != 0;
+  return on;
+}
+
 int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;

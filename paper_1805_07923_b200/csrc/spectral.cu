@@ -44,6 +44,8 @@ __device__ __forceinline__ double2 hshift(const double2* Yv, const double* eps_r
 __global__ void finalize_swe_kernel(PlanDev P, const double2* Y, long long y_mstride, int ldy,
                                     double2* out, long long out_mstride, int nonlin,
                                     double radius, int nmembers, RowFilter rf) {
+  pdl_wait();
+  pdl_trigger();
   const int R = P.R;
   const long long total = (long long)nmembers * (R + 1) * (R + 1);
   const long long plane = (long long)(R + 1) * (R + 1);
@@ -82,6 +84,8 @@ __global__ void finalize_swe_kernel(PlanDev P, const double2* Y, long long y_mst
 
 __global__ void finalize_divcurl_kernel(PlanDev P, const double2* Y, long long y_mstride, int ldy,
                                         double2* div, double2* curl, int nmembers) {
+  pdl_wait();
+  pdl_trigger();
   const int R = P.R;
   const long long plane = (long long)(R + 1) * (R + 1);
   const long long total = (long long)nmembers * plane;
@@ -109,6 +113,8 @@ __global__ void finalize_divcurl_kernel(PlanDev P, const double2* Y, long long y
 // state layout: [m][3][R+1][R+1] complex, fields (phi', zeta, delta)
 __global__ void eval_fi_kernel(int R, ModelConsts c, const double2* x, double2* out,
                                long long nmat, RowFilter rf) {
+  pdl_wait();
+  pdl_trigger();
   const long long plane = (long long)(R + 1) * (R + 1);
   const long long total = nmat * plane;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -130,6 +136,8 @@ __global__ void eval_fi_kernel(int R, ModelConsts c, const double2* x, double2* 
 
 __global__ void solve_kernel(int R, ModelConsts c, double beta, const double2* b, double2* out,
                              long long nmat, RowFilter rf) {
+  pdl_wait();
+  pdl_trigger();
   const long long plane = (long long)(R + 1) * (R + 1);
   const long long total = nmat * plane;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -153,6 +161,8 @@ __global__ void solve_kernel(int R, ModelConsts c, double beta, const double2* b
 }
 
 __global__ void combine_kernel(CombineArgs a, long long count) {
+  pdl_wait();
+  pdl_trigger();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
        i += (long long)gridDim.x * blockDim.x) {
     double acc = 0.0;
@@ -164,6 +174,8 @@ __global__ void combine_kernel(CombineArgs a, long long count) {
 
 __global__ void resize_kernel(const double2* in, int rin, double2* out, int rout, long long nmat,
                               RowFilter rf) {
+  pdl_wait();
+  pdl_trigger();
   const long long plane = (long long)(rout + 1) * (rout + 1);
   const long long total = nmat * plane;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -186,6 +198,8 @@ constexpr int kUp = 4;
 __global__ void __launch_bounds__(256) upload_triangle_kernel(const double2* __restrict__ host,
                                                               double2* __restrict__ out, int R,
                                                               long long total) {
+  pdl_wait();
+  pdl_trigger();
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < total;
        base += stride * kUp) {
@@ -213,6 +227,8 @@ __global__ void __launch_bounds__(256) upload_triangle_kernel(const double2* __r
 __global__ void __launch_bounds__(256) download_triangle_kernel(const double2* __restrict__ dev,
                                                                 double2* __restrict__ host, int R,
                                                                 long long total, int write_lower) {
+  pdl_wait();
+  pdl_trigger();
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < total;
        base += stride * kUp) {
@@ -239,6 +255,8 @@ __global__ void __launch_bounds__(256) download_triangle_kernel(const double2* _
 }
 
 __global__ void spec_combine_kernel(SpecCombineArgs a, long long nmat, RowFilter rf) {
+  pdl_wait();
+  pdl_trigger();
   const int ro = a.rout;
   const long long plane = (long long)(ro + 1) * (ro + 1);
   const long long total = nmat * plane;
@@ -264,6 +282,8 @@ __global__ void spec_combine_kernel(SpecCombineArgs a, long long nmat, RowFilter
 // b = sum_k w_k x_k -> theta = (I - beta F_I)^-1 b -> fi = L_G(theta)
 __global__ void sweep_node_kernel(int R, ModelConsts c, double beta, SpecCombineArgs a,
                                   double2* theta, double2* fi, long long nstates, RowFilter rf) {
+  pdl_wait();
+  pdl_trigger();
   const long long plane = (long long)(R + 1) * (R + 1);
   const long long total = nstates * plane;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -316,8 +336,7 @@ int launch_finalize_swe(const PlanDev& P, const double2* Y, long long y_mstride,
                         int nmembers, cudaStream_t st, RowFilter rf) {
   const long long n = (long long)nmembers * (P.R + 1) * (P.R + 1);
   StageScope sc("finalize_swe", st);
-  finalize_swe_kernel<<<grid_for(n, 256), 256, 0, st>>>(P, Y, y_mstride, ldy, out, out_mstride,
-                                                        nonlin ? 1 : 0, radius, nmembers, rf);
+  SW_CUDA(launch_pdl(finalize_swe_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, P, Y, y_mstride, ldy, out, out_mstride, nonlin ? 1 : 0, radius, nmembers, rf));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -326,8 +345,7 @@ int launch_finalize_divcurl(const PlanDev& P, const double2* Y, long long y_mstr
                             double2* div, double2* curl, int nmembers, cudaStream_t st) {
   const long long n = (long long)nmembers * (P.R + 1) * (P.R + 1);
   StageScope sc("finalize_divcurl", st);
-  finalize_divcurl_kernel<<<grid_for(n, 256), 256, 0, st>>>(P, Y, y_mstride, ldy, div, curl,
-                                                            nmembers);
+  SW_CUDA(launch_pdl(finalize_divcurl_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, P, Y, y_mstride, ldy, div, curl, nmembers));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -336,7 +354,7 @@ int launch_eval_fi(int R, const ModelConsts& c, const double2* x, double2* out, 
                    cudaStream_t st) {
   const long long n = nmat * (R + 1) * (R + 1);
   StageScope sc("eval_fi", st);
-  eval_fi_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, x, out, nmat, current_row_filter());
+  SW_CUDA(launch_pdl(eval_fi_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, R, c, x, out, nmat, current_row_filter()));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -345,14 +363,14 @@ int launch_solve(int R, const ModelConsts& c, double beta, const double2* b, dou
                  long long nmat, cudaStream_t st) {
   const long long n = nmat * (R + 1) * (R + 1);
   StageScope sc("solve_implicit", st);
-  solve_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, beta, b, out, nmat, current_row_filter());
+  SW_CUDA(launch_pdl(solve_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, R, c, beta, b, out, nmat, current_row_filter()));
   SW_LAUNCH_CHECK();
   return kOk;
 }
 
 int launch_combine(const CombineArgs& a, long long count, cudaStream_t st) {
   StageScope sc("combine", st);
-  combine_kernel<<<grid_for(count, 256), 256, 0, st>>>(a, count);
+  SW_CUDA(launch_pdl(combine_kernel, dim3(grid_for(count, 256)), dim3(256), 0, st, a, count));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -360,7 +378,7 @@ int launch_combine(const CombineArgs& a, long long count, cudaStream_t st) {
 int launch_spec_combine(const SpecCombineArgs& a, long long nmat, cudaStream_t st) {
   const long long n = nmat * (a.rout + 1) * (a.rout + 1);
   StageScope sc("spec_combine", st);
-  spec_combine_kernel<<<grid_for(n, 256), 256, 0, st>>>(a, nmat, current_row_filter());
+  SW_CUDA(launch_pdl(spec_combine_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, a, nmat, current_row_filter()));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -369,8 +387,7 @@ int launch_sweep_node(int R, const ModelConsts& c, double beta, const SpecCombin
                       double2* theta, double2* fi, long long nstates, cudaStream_t st) {
   const long long n = nstates * (R + 1) * (R + 1);
   StageScope sc("sweep_node", st);
-  sweep_node_kernel<<<grid_for(n, 256), 256, 0, st>>>(R, c, beta, a, theta, fi, nstates,
-                                                       current_row_filter());
+  SW_CUDA(launch_pdl(sweep_node_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, R, c, beta, a, theta, fi, nstates, current_row_filter()));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -379,7 +396,7 @@ int launch_resize(const double2* in, int rin, double2* out, int rout, long long 
                   cudaStream_t st) {
   const long long n = nmat * (rout + 1) * (rout + 1);
   StageScope sc("resize", st);
-  resize_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, rin, out, rout, nmat, current_row_filter());
+  SW_CUDA(launch_pdl(resize_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, in, rin, out, rout, nmat, current_row_filter()));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -395,12 +412,14 @@ int launch_upload_triangle(const double2* host, double2* out, int R, long long n
   static const int cap = std::max(1, env_int("SWSDC_UPLOAD_CTAS", 32));
   const long long want = (n + 256LL * kUp - 1) / (256LL * kUp);
   const int blocks = (int)std::min<long long>(want, cap);
-  upload_triangle_kernel<<<blocks, 256, 0, st>>>(host, out, R, n);
+  SW_CUDA(launch_pdl(upload_triangle_kernel, dim3(blocks), dim3(256), 0, st, host, out, R, n));
   SW_LAUNCH_CHECK();
   return kOk;
 }
 
 __global__ void zero_lower_kernel(double2* out, int R, long long nmat) {
+  pdl_wait();
+  pdl_trigger();
   const long long total = nmat * (R + 1) * (R + 1);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -413,7 +432,7 @@ __global__ void zero_lower_kernel(double2* out, int R, long long nmat) {
 int launch_zero_lower(double2* out, int R, long long nmat, cudaStream_t st) {
   const long long n = nmat * (R + 1) * (R + 1);
   StageScope sc("zero_lower", st);
-  zero_lower_kernel<<<grid_for(n, 256), 256, 0, st>>>(out, R, nmat);
+  SW_CUDA(launch_pdl(zero_lower_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, out, R, nmat));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -425,7 +444,7 @@ int launch_download_triangle(const double2* dev, double2* host, int R, long long
   static const int cap = std::max(1, env_int("SWSDC_UPLOAD_CTAS", 32));
   const long long want = (n + 256LL * kUp - 1) / (256LL * kUp);
   const int blocks = (int)std::min<long long>(want, cap);
-  download_triangle_kernel<<<blocks, 256, 0, st>>>(dev, host, R, n, write_lower);
+  SW_CUDA(launch_pdl(download_triangle_kernel, dim3(blocks), dim3(256), 0, st, dev, host, R, n, write_lower));
   SW_LAUNCH_CHECK();
   return kOk;
 }
