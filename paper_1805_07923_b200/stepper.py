@@ -22,11 +22,12 @@ from .swe import EvalCounters, PrognosticState
 
 
 class InstabilityError(RuntimeError):
-    """Non-finite state after a step (harness.py:31-36)."""
+    """Non-finite state after step `step` (0-based, as the reference's
+    run_simulation loop index; harness.py:31-36)."""
 
-    def __init__(self, step: int):
+    def __init__(self, step: int, message: str | None = None):
         self.step = step
-        super().__init__(f"non-finite state after step {step}")
+        super().__init__(message or f"non-finite state after step {step}")
 
 
 def _counter_sum(levels) -> list[EvalCounters]:
@@ -123,7 +124,7 @@ class MLSDCStepper:
             flags[k].copy_(self._g.flag)
         bad = torch.nonzero(~flags)
         if bad.numel():
-            raise InstabilityError(int(bad[0]) + 1)
+            raise InstabilityError(int(bad[0]))
         return self.state
 
     @property
@@ -162,5 +163,5 @@ class SDCStepper:
             flags[k].copy_(self._g.flag)
         bad = torch.nonzero(~flags)
         if bad.numel():
-            raise InstabilityError(int(bad[0]) + 1)
+            raise InstabilityError(int(bad[0]))
         return self.state

@@ -23,6 +23,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, REPO)
+sys.path.insert(0, HERE)
 
 from swsdc import mlsdc, sdc, spharm  # noqa: E402  (reference, read-only)
 from swsdc.swe import ModelParams, PrognosticState, ShallowWaterRHS  # noqa: E402
@@ -194,7 +195,48 @@ def gen_config0():
     np.savez_compressed(os.path.join(HERE, "config0.npz"), x=x, out=from_ps(y))
 
 
+from harness_runs import HARNESS_RUNS  # noqa: E402  (shared with tests/test_harness_host.py)
+
+
+def gen_harness():
+    """test-case initial states (reference testcases.py) and short
+    run_simulation runs of every scheme with their cost counters, error norms
+    and spectra (reference harness.py)."""
+    from swsdc import harness, testcases  # reference, read-only
+    out = {}
+    R = 21
+    n_lon, n_lat = spharm.default_grid_shape(R)
+    plan = spharm.TransformPlan(spharm.build_gaussian_grid(n_lat, n_lon), R)
+    for kind in testcases.CASE_KINDS:
+        st, prm = testcases.build_initial_state(testcases.TestCaseSpec(kind), plan)
+        out[f"init_{kind}"] = from_ps(st)
+        out[f"init_{kind}_hbar"] = np.float64(prm.h_bar)
+    states = {}
+    for name, (case, scheme, rf, dt, t_end, it, nf, nc, alpha) in HARNESS_RUNS.items():
+        cfg = harness.RunConfig(testcase=testcases.TestCaseSpec(case), scheme=scheme, r_fine=rf,
+                                dt=dt, t_end=t_end, iterations=it, nodes_fine=nf,
+                                nodes_coarse=nc, alpha=alpha)
+        res = harness.run_simulation(cfg)
+        states[name] = res.state
+        out[f"run_{name}_state"] = from_ps(res.state)
+        c = res.cost
+        out[f"run_{name}_cost"] = np.array(
+            [[x.solves, x.implicit_evals, x.explicit_evals]
+             for x in (c.fine, c.coarse, c.fine_predicted, c.coarse_predicted, c.fine_init,
+                       c.coarse_init)], dtype=np.int64)
+        out[f"run_{name}_speedup"] = np.float64(c.theoretical_speedup or 0.0)
+    rep = harness.compute_error_norms(states["sdc_dome"], states["irk2_rh"], plan)
+    out["err_linf"] = np.array([rep.linf[v] for v in harness.STATE_VARS])
+    out["err_l2"] = np.array([rep.l2[v] for v in harness.STATE_VARS])
+    out["spectrum_zeta"] = harness.max_spectrum(states["mlsdc_jet"].zeta)
+    np.savez_compressed(os.path.join(HERE, "harness.npz"), **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "harness":
+        gen_harness()
+        sys.exit(0)
+    gen_harness()
     gen_grids()
     gen_transforms()
     gen_rhs()
