@@ -323,6 +323,8 @@ int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, dou
     a.work = sh ? sh->work[which][ls] : p->work[which][ls];
     a.out_mstride = out_mstride;
     a.nmembers = nmembers;
+    static const int short_tiles = env_int("SWSDC_ANA_SHORT", 1);
+    a.short_tiles = short_tiles;
     const int nw = sh ? sh->nwork[which][ls] : p->nwork[which][ls];
     if (nw == 0) continue;
     SW_TRY(launch_analysis(P, a, nw, lsplit, st));

@@ -25,6 +25,8 @@
 // Analysis: the q tile (32 degrees x 128 latitudes) is generated into shared
 // memory and contracted over latitude with FP64 tensor-core DMMA
 // (mma.sync.m8n8k4.f64), so the latitude reduction happens inside the MMA.
+#include <type_traits>
+
 #include "common.cuh"
 #include "legendre.cuh"
 
@@ -540,6 +542,11 @@ ana_kernel(PlanDev P, AnaArgs a) {
       if (jh0 < P.Jh) { sd_nx = seeds[jh0]; mu_nx = P.mu_n[jh0]; }
     }
     int ks = 0;
+    // a row's last chunk with <= 16 degrees has an empty upper m-tile (degrees
+    // 16..31 of the chunk): its warps run an instantiation without those DMMAs
+    // and recurrence steps (decided once per warp, outside the unrolled loops)
+    auto blocks = [&](auto mt_count) {
+    constexpr int MTN = decltype(mt_count)::value;
     for (int jb32 = half; jb32 < nblk; jb32 += LSPLIT) {
       __syncwarp();
       // regenerate q for 32 degrees at latitude jh = 32*jb32 + lane
@@ -555,7 +562,7 @@ ana_kernel(PlanDev P, AnaArgs a) {
         qs[lane] = qa;
         qs[16 * kQS + lane] = qb;
 #pragma unroll
-        for (int kk = 2; kk < kChunk; kk += 2) {
+        for (int kk = 2; kk < (MTN == 2 ? kChunk : kChunk / 2); kk += 2) {
           qa = fma(mu, qb, -bs[kk] * qa);
           qb = fma(mu, qa, -bs[kk + 1] * qb);
           qs[(kk >> 1) * kQS + lane] = qa;
@@ -584,7 +591,7 @@ ana_kernel(PlanDev P, AnaArgs a) {
 #pragma unroll
         for (int p = 0; p < 2; ++p)
 #pragma unroll
-          for (int mt = 0; mt < 2; ++mt) {
+          for (int mt = 0; mt < MTN; ++mt) {
             const double av = qs[(p * 16 + mt * 8 + g) * kQS + s * 4 + t];
 #pragma unroll
             for (int n = 0; n < NT; ++n) dmma884(acc[p][mt][n], av, bv[p][n]);
@@ -592,6 +599,9 @@ ana_kernel(PlanDev P, AnaArgs a) {
         __syncwarp();   // this slot is refilled kBDepth - 1 k-steps later
       }
     }
+    };
+    if (a.short_tiles && nout - k0 <= kChunk / 2) blocks(std::integral_constant<int, 1>());
+    else blocks(std::integral_constant<int, 2>());
     cp_async_wait<0>();
   }
 

@@ -39,6 +39,7 @@ struct AnaArgs {
   const int2* work;        // (r, first chunk) list, one CTA (ana_warps_per_cta chunks) each
   long long out_mstride;   // complex elements between members (blockIdx.y)
   int nmembers;
+  int short_tiles;         // run half-empty last chunks without their upper m-tile
 };
 
 int build_checkpoints(const PlanDev& P, const double* a_tab, const double* b_tab,
