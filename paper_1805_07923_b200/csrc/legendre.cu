@@ -661,10 +661,203 @@ ana_kernel(PlanDev P, AnaArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Analysis on the FP64 vector pipe (DFMA), for the DMMA-vs-DFMA comparison the
+// north star asks for (SWSDC_ANA_DFMA=1).  Same decomposition as ana_kernel
+// (work lists, wave-fitted latitude split, q tile, cp.async x ring); lane =
+// degree slot of the chunk (lanes 0..15 even degrees, 16..31 odd), holding the
+// 4 NT vectors' accumulators.  Per k-step (4 latitudes) a lane reads its q row
+// segment (2 x 16 B) and, per vector, the real and imaginary x values of the 4
+// latitudes (2 x 16 B half-warp broadcasts: S for even, D for odd degrees).
+// ---------------------------------------------------------------------------
+constexpr int kQD = kChunk + 2;   // q row stride (doubles): 16-B aligned, conflict-free rows
+template <int NT>
+__host__ __device__ constexpr int anad_warp_doubles() {
+  return kChunk * kQD + kChunk + kBDepth * 2 * NT * 32;
+}
+
+template <int NT, int LSPLIT>
+__global__ void __launch_bounds__(kAnaWarps * 32)
+ana_dfma_kernel(PlanDev P, AnaArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(16) double smem[];
+  constexpr int kWD = anad_warp_doubles<NT>();
+  constexpr int NV = 4 * NT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* qs = smem + (size_t)warp * kWD;     // [32 degree slots][kQD latitudes]
+  double* bs = qs + kChunk * kQD;
+  double* bring = bs + kChunk;                // [kBDepth][2][NT * 32]
+  const double* x = a.x + (size_t)blockIdx.y * a.xl.mstride;
+  double2* out = a.out + (size_t)blockIdx.y * a.out_mstride;
+  const int2 wk = a.work[blockIdx.x];
+  const int r = wk.x, c = wk.y + warp / LSPLIT, half = warp % LSPLIT;
+  const int nout = a.smax - r + 1;
+  if (a.zero_fill && wk.y == 0 && warp == 0) {
+    for (int idx = lane; idx < a.nv * r; idx += 32) {
+      const int v = idx / r, s = idx - v * r;
+      out[(size_t)v * a.out_vstride + (size_t)r * a.out_rstride + s] = make_double2(0.0, 0.0);
+    }
+  }
+  const bool active = c * kChunk < nout;
+  const int k0 = c * kChunk;
+  const int par = lane >> 4;   // degree parity of this lane: x parity S (0) or D (1)
+  double acc[NV][2];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) { acc[v][0] = 0.0; acc[v][1] = 0.0; }
+  if (active) {
+    bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
+    const double2* seeds = P.ckpt + (size_t)(P.ck_off[r] + c) * P.Jh;
+    const int nc = a.xl.nc, jh4 = a.xl.jh4;
+    const double* xr = x + (size_t)r * jh4 * 2 * nc * 4;
+    const int nblk = (P.Jh + 31) >> 5;
+    const int nmine = (nblk - half + LSPLIT - 1) / LSPLIT;
+    const int nks = nmine * 8;
+    auto issue = [&](int ks) {
+      if (ks < nks) {
+        const int jb = ((half + (ks >> 3) * LSPLIT) << 3) + (ks & 7);
+        if (jb < jh4) {
+          double* dst = bring + (ks % kBDepth) * (2 * NT * 32);
+#pragma unroll
+          for (int cc = lane; cc < 2 * NT * 16; cc += 32) {
+            const int p = cc / (NT * 16), q = cc - p * (NT * 16);
+            cp_async16_ana(dst + p * NT * 32 + 2 * q, xr + ((size_t)jb * 2 + p) * nc * 4 + 2 * q);
+          }
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int d = 0; d < kBDepth - 1; ++d) issue(d);
+    double2 sd_nx = make_double2(0.0, 0.0);
+    double mu_nx = 0.0;
+    {
+      const int jh0 = (half << 5) + lane;
+      if (jh0 < P.Jh) { sd_nx = seeds[jh0]; mu_nx = P.mu_n[jh0]; }
+    }
+    int ks = 0;
+    for (int jb32 = half; jb32 < nblk; jb32 += LSPLIT) {
+      __syncwarp();
+      // q tile: lane = latitude writes its column; row = degree slot (even rows 0..15, odd 16..31)
+      const int jh = (jb32 << 5) + lane;
+      const double2 sd = sd_nx;
+      const double mu = mu_nx;
+      {
+        const int jn = ((jb32 + LSPLIT) << 5) + lane;
+        if (jn < P.Jh) { sd_nx = seeds[jn]; mu_nx = P.mu_n[jn]; }
+      }
+      double qa = 0.0, qb = 0.0;
+      if (jh < P.Jh) { qa = sd.x; qb = sd.y; }
+      qs[lane] = qa;
+      qs[16 * kQD + lane] = qb;
+#pragma unroll
+      for (int kk = 2; kk < kChunk; kk += 2) {
+        qa = fma(mu, qb, -bs[kk] * qa);
+        qb = fma(mu, qa, -bs[kk + 1] * qb);
+        qs[(kk >> 1) * kQD + lane] = qa;
+        qs[(16 + (kk >> 1)) * kQD + lane] = qb;
+      }
+      __syncwarp();
+      const double* qrow = qs + (size_t)((par << 4) + (lane & 15)) * kQD;
+#pragma unroll 1
+      for (int s = 0; s < 8; ++s, ++ks) {
+        issue(ks + kBDepth - 1);
+        cp_async_wait<kBDepth - 1>();
+        __syncwarp();
+        const double* bsrc = bring + (ks % kBDepth) * (2 * NT * 32) + par * NT * 32;
+        const int lat0 = ((jb32 << 3) + s) * 4;
+        const double2 q01 = *reinterpret_cast<const double2*>(qrow + s * 4);
+        const double2 q23 = *reinterpret_cast<const double2*>(qrow + s * 4 + 2);
+        if (lat0 + 3 < P.Jh) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+#pragma unroll
+            for (int ri = 0; ri < 2; ++ri) {
+              const int col = 2 * v + ri;
+              const double* xc = bsrc + (col >> 3) * 32 + (col & 7) * 4;
+              const double2 x01 = *reinterpret_cast<const double2*>(xc);
+              const double2 x23 = *reinterpret_cast<const double2*>(xc + 2);
+              double t = acc[v][ri];
+              t = fma(q01.x, x01.x, t);
+              t = fma(q01.y, x01.y, t);
+              t = fma(q23.x, x23.x, t);
+              acc[v][ri] = fma(q23.y, x23.y, t);
+            }
+          }
+        } else {
+          // last latitude block with padding: padded x entries may be garbage
+          const double qv[4] = {q01.x, q01.y, q23.x, q23.y};
+#pragma unroll
+          for (int tt = 0; tt < 4; ++tt) {
+            if (lat0 + tt >= P.Jh) break;
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+#pragma unroll
+              for (int ri = 0; ri < 2; ++ri) {
+                const int col = 2 * v + ri;
+                acc[v][ri] = fma(qv[tt], bsrc[(col >> 3) * 32 + (col & 7) * 4 + tt], acc[v][ri]);
+              }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    cp_async_wait<0>();
+  }
+  if (LSPLIT > 1) {
+    const unsigned bar_id = 1 + warp / LSPLIT, bar_n = 32 * LSPLIT;
+    asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
+    double* red = smem + (size_t)warp * kWD;
+    if (half > 0 && active) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        red[(2 * v) * 32 + lane] = acc[v][0];
+        red[(2 * v + 1) * 32 + lane] = acc[v][1];
+      }
+    }
+    asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
+    if (half > 0 || !active) return;
+    for (int h = 1; h < LSPLIT; ++h) {
+      const double* src = smem + (size_t)(warp + h) * kWD;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        acc[v][0] += src[(2 * v) * 32 + lane];
+        acc[v][1] += src[(2 * v + 1) * 32 + lane];
+      }
+    }
+  } else if (!active) {
+    return;
+  }
+  // lane -> degree k = k0 + par + 2 (lane & 15)
+  const int k = k0 + par + 2 * (lane & 15);
+  if (k < nout) {
+    const double gs = P.gsc[(size_t)r * P.ldk + k];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      if (v < a.nv)
+        out[(size_t)v * a.out_vstride + (size_t)r * a.out_rstride + r + k] =
+            make_double2(acc[v][0] * gs, acc[v][1] * gs);
+  }
+}
+
 // CTA = ana_chunks_per_cta(LSPLIT) chunks x LSPLIT latitude splits.
+bool ana_dfma() {
+  static const int knob = env_int("SWSDC_ANA_DFMA", 0);
+  return knob != 0;
+}
+
 template <int NT, int LSPLIT>
 int launch_ana_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st) {
   const int warps = LSPLIT * ana_chunks_per_cta(LSPLIT);
+  if (ana_dfma()) {
+    const size_t smem = sizeof(double) * warps * anad_warp_doubles<NT>();
+    auto kern = ana_dfma_kernel<NT, LSPLIT>;
+    SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
+    StageScope sc("legendre_analysis", st);
+    SW_CUDA(launch_pdl(kern, dim3(nwork, a.nmembers), dim3(warps * 32), smem, st, P, a));
+    SW_LAUNCH_CHECK();
+    return kOk;
+  }
   const size_t smem = sizeof(double) * warps * ana_warp_doubles<NT>();
   auto kern = ana_kernel<NT, LSPLIT>;
   SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
@@ -687,8 +880,9 @@ int launch_ana_nt(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, cud
 template <int NT, int LSPLIT>
 int ana_ctas_per_sm_t() {
   const int warps = LSPLIT * ana_chunks_per_cta(LSPLIT);
-  const size_t smem = sizeof(double) * warps * ana_warp_doubles<NT>();
-  auto kern = ana_kernel<NT, LSPLIT>;
+  const bool dfma = ana_dfma();
+  const size_t smem = sizeof(double) * warps * (dfma ? anad_warp_doubles<NT>() : ana_warp_doubles<NT>());
+  auto kern = dfma ? ana_dfma_kernel<NT, LSPLIT> : ana_kernel<NT, LSPLIT>;
   if (set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem) != kOk) return 1;
   int n = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, warps * 32, smem) != cudaSuccess) {

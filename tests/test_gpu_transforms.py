@@ -112,9 +112,10 @@ def test_pinned_host_upload_and_download(golden):
 
 
 def test_tma_and_forced_split_variants_match_reference(tmp_path):
-    """The opt-in TMA analysis (SWSDC_ANA_TMA=2) and every forced latitude split
-    (SWSDC_ANA_LSPLIT=1..4) give the reference's analysis; the knobs are read once
-    per process, so each variant runs in a subprocess."""
+    """The opt-in TMA analysis (SWSDC_ANA_TMA=2), the DFMA analysis kept for the
+    DMMA-vs-DFMA comparison (SWSDC_ANA_DFMA=1), every forced latitude split
+    (SWSDC_ANA_LSPLIT=1..4) and the unspecialised last chunk give the reference's
+    analysis; the knobs are read once per process, so each runs in a subprocess."""
     import subprocess
     import sys
     code = (
@@ -132,7 +133,8 @@ def test_tma_and_forced_split_variants_match_reference(tmp_path):
         "print(worst)\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     for env in ({"SWSDC_ANA_TMA": "2"}, {"SWSDC_ANA_LSPLIT": "1"}, {"SWSDC_ANA_LSPLIT": "2"},
-                {"SWSDC_ANA_LSPLIT": "3"}, {"SWSDC_ANA_LSPLIT": "4"}):
+                {"SWSDC_ANA_LSPLIT": "3"}, {"SWSDC_ANA_LSPLIT": "4"}, {"SWSDC_ANA_DFMA": "1"},
+                {"SWSDC_ANA_DFMA": "1", "SWSDC_ANA_LSPLIT": "3"}, {"SWSDC_ANA_SHORT": "0"}):
         out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True,
                              text=True, env={**os.environ, **env}, timeout=300)
         assert out.returncode == 0, out.stderr[-2000:]
