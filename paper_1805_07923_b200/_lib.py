@@ -13,7 +13,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libswsdc_b200.so")
+# SWSDC_LIB: load another build of the library (same-box A/B of kernel changes)
+LIB_PATH = os.environ.get("SWSDC_LIB") or os.path.join(_HERE, "libswsdc_b200.so")
 
 _lib = None
 

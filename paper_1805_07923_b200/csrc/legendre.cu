@@ -511,7 +511,6 @@ ana_kernel(PlanDev P, AnaArgs a) {
   if (active) {
     bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
     const double2* seeds = P.ckpt + (size_t)(P.ck_off[r] + c) * P.Jh;
-    const int ncol = 2 * a.nv;
     const int nc = a.xl.nc, jh4 = a.xl.jh4;
     const double* xr = x + (size_t)r * jh4 * 2 * nc * 4;
     const int nblk = (P.Jh + 31) >> 5;
@@ -579,15 +578,28 @@ ana_kernel(PlanDev P, AnaArgs a) {
         cp_async_wait<kBDepth - 1>();
         __syncwarp();
         const double* bsrc = bring + (ks % kBDepth) * (2 * NT * 32);
-        const bool ok = (((jb32 << 3) + s) * 4 + t) < P.Jh;
+        // Columns need no mask: column n of D depends only on column n of B, and
+        // columns >= 2 nv only feed accumulators that are never written.  Rows
+        // (latitudes) past Jh meet q = 0 there, but the padded x entries (or a
+        // stale ring slot past the row's last block) may hold non-finite bits,
+        // so k-steps reaching past Jh take the masked loads (warp-uniform test).
+        const int lat0 = ((jb32 << 3) + s) * 4;
         double bv[2][NT];
+        if (lat0 + 4 <= P.Jh) {
 #pragma unroll
-        for (int p = 0; p < 2; ++p)
+          for (int p = 0; p < 2; ++p)
 #pragma unroll
-          for (int n = 0; n < NT; ++n) {
-            const double b = bsrc[p * NT * 32 + n * 32 + lane];
-            bv[p][n] = (ok && (n * 8 + g) < ncol) ? b : 0.0;
-          }
+            for (int n = 0; n < NT; ++n) bv[p][n] = bsrc[p * NT * 32 + n * 32 + lane];
+        } else {
+          const bool ok = lat0 + t < P.Jh;
+#pragma unroll
+          for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+              const double b = bsrc[p * NT * 32 + n * 32 + lane];
+              bv[p][n] = ok ? b : 0.0;
+            }
+        }
 #pragma unroll
         for (int p = 0; p < 2; ++p)
 #pragma unroll
