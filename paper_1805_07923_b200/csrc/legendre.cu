@@ -516,23 +516,54 @@ ana_kernel(PlanDev P, AnaArgs a) {
     const int nblk = (P.Jh + 31) >> 5;
     const int nmine = (nblk - half + LSPLIT - 1) / LSPLIT;   // latitude blocks of this warp
     const int nks = nmine * 8;
-    // k-step ks -> 4-latitude block jb; copies of blocks past the row end are skipped
-    auto issue = [&](int ks) {
-      if (ks < nks) {
-        const int jb = ((half + (ks >> 3) * LSPLIT) << 3) + (ks & 7);
-        if (jb < jh4) {
-          double* dst = bring + (ks % kBDepth) * (2 * NT * 32);
+    // Issue side of the x ring: k-steps are issued in order; consecutive k-steps
+    // of a latitude block are consecutive 4-latitude blocks jb, this warp's
+    // blocks are LSPLIT apart.  A running jb replaces per-step index math, the
+    // per-lane copy offsets are loop-invariant, and copies stop at the row's
+    // last block (jb < jh4) or after the warp's last k-step.
+    static_assert((kBDepth & (kBDepth - 1)) == 0, "ring depth must be a power of 2");
+    constexpr int kCp = (2 * NT * 16 + 31) / 32;   // 16-byte copies per lane per k-step
+    int coff_d[kCp], coff_s[kCp];
 #pragma unroll
-          for (int cc = lane; cc < 2 * NT * 16; cc += 32) {
-            const int p = cc / (NT * 16), q = cc - p * (NT * 16);
-            cp_async16_ana(dst + p * NT * 32 + 2 * q, xr + ((size_t)jb * 2 + p) * nc * 4 + 2 * q);
+    for (int u = 0; u < kCp; ++u) {
+      const int cc = lane + 32 * u;
+      const int p = cc / (NT * 16), q = cc - p * (NT * 16);
+      coff_d[u] = (cc < 2 * NT * 16) ? p * NT * 32 + 2 * q : -1;
+      coff_s[u] = p * nc * 4 + 2 * q;
+    }
+    const size_t jb_stride = (size_t)2 * nc * 4;
+    const size_t jump = (size_t)((LSPLIT - 1) * 8 + 1) * jb_stride;
+    const size_t poff = (size_t)nc * 4;                       // parity-1 half of a block
+    const double* ip = xr + (size_t)(half << 3) * jb_stride;  // block of the next issue
+    int iss = 0, ijb = half << 3;
+    auto issue_next = [&]() {
+      if (iss < nks && ijb < jh4) {
+        double* dst = bring + (iss & (kBDepth - 1)) * (2 * NT * 32);
+        if constexpr (NT % 2 == 0) {
+          // each parity half is NT/2 copies per lane at fixed offsets from the
+          // lane's base: immediate-offset addressing, no per-step index math
+          const double* s0 = ip + 2 * lane;
+          const double* s1 = s0 + poff;
+          double* d0 = dst + 2 * lane;
+#pragma unroll
+          for (int u = 0; u < NT / 2; ++u) {
+            cp_async16_ana(d0 + 64 * u, s0 + 64 * u);
+            cp_async16_ana(d0 + NT * 32 + 64 * u, s1 + 64 * u);
           }
+        } else {
+#pragma unroll
+          for (int u = 0; u < kCp; ++u)
+            if (coff_d[u] >= 0) cp_async16_ana(dst + coff_d[u], ip + coff_s[u]);
         }
       }
       cp_async_commit();
+      ++iss;
+      const bool blk = (iss & 7) == 0;
+      ijb += blk ? (LSPLIT - 1) * 8 + 1 : 1;
+      ip += blk ? jump : jb_stride;
     };
 #pragma unroll
-    for (int d = 0; d < kBDepth - 1; ++d) issue(d);
+    for (int d = 0; d < kBDepth - 1; ++d) issue_next();
     // seed and mu of this lane's latitude in the next block, fetched one block ahead
     double2 sd_nx = make_double2(0.0, 0.0);
     double mu_nx = 0.0;
@@ -572,44 +603,40 @@ ana_kernel(PlanDev P, AnaArgs a) {
         for (int kk = 0; kk < kChunk; ++kk) qs[((kk & 1) * 16 + (kk >> 1)) * kQS + lane] = 0.0;
       }
       __syncwarp();
+      // k-steps of this block; blocks reaching past Jh (padding rows of x may
+      // hold non-finite bits, q = 0 there) take the masked instantiation
+      auto ksteps = [&](auto full_c) {
+        constexpr bool FULL = decltype(full_c)::value;
 #pragma unroll
-      for (int s = 0; s < 8; ++s, ++ks) {
-        issue(ks + kBDepth - 1);
-        cp_async_wait<kBDepth - 1>();
-        __syncwarp();
-        const double* bsrc = bring + (ks % kBDepth) * (2 * NT * 32);
-        // Columns need no mask: column n of D depends only on column n of B, and
-        // columns >= 2 nv only feed accumulators that are never written.  Rows
-        // (latitudes) past Jh meet q = 0 there, but the padded x entries (or a
-        // stale ring slot past the row's last block) may hold non-finite bits,
-        // so k-steps reaching past Jh take the masked loads (warp-uniform test).
-        const int lat0 = ((jb32 << 3) + s) * 4;
-        double bv[2][NT];
-        if (lat0 + 4 <= P.Jh) {
-#pragma unroll
-          for (int p = 0; p < 2; ++p)
-#pragma unroll
-            for (int n = 0; n < NT; ++n) bv[p][n] = bsrc[p * NT * 32 + n * 32 + lane];
-        } else {
-          const bool ok = lat0 + t < P.Jh;
+        for (int s = 0; s < 8; ++s, ++ks) {
+          issue_next();
+          cp_async_wait<kBDepth - 1>();
+          __syncwarp();
+          // no column mask: column n of D depends only on column n of B, and
+          // columns >= 2 nv only feed accumulators that are never written
+          const double* bsrc = bring + (ks & (kBDepth - 1)) * (2 * NT * 32);
+          double bv[2][NT];
+          const bool ok = FULL || (((jb32 << 3) + s) * 4 + t) < P.Jh;
 #pragma unroll
           for (int p = 0; p < 2; ++p)
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
               const double b = bsrc[p * NT * 32 + n * 32 + lane];
-              bv[p][n] = ok ? b : 0.0;
+              bv[p][n] = FULL ? b : (ok ? b : 0.0);
             }
+#pragma unroll
+          for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int mt = 0; mt < MTN; ++mt) {
+              const double av = qs[(p * 16 + mt * 8 + g) * kQS + s * 4 + t];
+#pragma unroll
+              for (int n = 0; n < NT; ++n) dmma884(acc[p][mt][n], av, bv[p][n]);
+            }
+          __syncwarp();   // this slot is refilled kBDepth - 1 k-steps later
         }
-#pragma unroll
-        for (int p = 0; p < 2; ++p)
-#pragma unroll
-          for (int mt = 0; mt < MTN; ++mt) {
-            const double av = qs[(p * 16 + mt * 8 + g) * kQS + s * 4 + t];
-#pragma unroll
-            for (int n = 0; n < NT; ++n) dmma884(acc[p][mt][n], av, bv[p][n]);
-          }
-        __syncwarp();   // this slot is refilled kBDepth - 1 k-steps later
-      }
+      };
+      if ((jb32 << 5) + 32 <= P.Jh) ksteps(std::true_type());
+      else ksteps(std::false_type());
     }
     };
     if (a.short_tiles && nout - k0 <= kChunk / 2) blocks(std::integral_constant<int, 1>());
