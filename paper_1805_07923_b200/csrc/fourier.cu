@@ -26,11 +26,14 @@
 #include <algorithm>
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "fourier.cuh"
 #include "reg_fft.cuh"
 
 namespace swsdc {
+namespace cg = cooperative_groups;
 namespace {
 
 constexpr int kSweMaxPts = 4;   // grid points per thread in the fused SWE kernel
@@ -457,41 +460,48 @@ __global__ void SWSDC_REG_BOUNDS(K) g2f_reg_kernel(PlanDev P, const double* grid
   }
 }
 
-// Output stage shared by the fused SWE kernels: weighted analysis vectors of
-// the 7 (or 2) forward-transformed product rings (natural order) into x.
+// Output stage shared by the fused SWE kernels: weighted analysis vectors at
+// wavenumber r of latitude pair jh from its 7 (or 2) forward-transformed
+// product rings (natural order) into x.
+template <bool NONLIN>
+__device__ __forceinline__ void swe_out_one(const double2* rings, const PlanDev& P, double* xm,
+                                            const XLayout& xl, int r, int jh, double w, double wc,
+                                            double ia, bool eq) {
+  const int RS = P.ring_stride;
+  double2 A1n, A1s, A2n, A2s;
+  get_pair(rings, P, r, A1n, A1s);
+  get_pair(rings + RS, P, r, A2n, A2s);
+  if (!NONLIN) {
+    put_x(xm, xl, 0, r, jh, cscale(A1n, w), cscale(A1s, w), eq);
+    put_x(xm, xl, 1, r, jh, cscale(A2n, w), cscale(A2s, w), eq);
+  } else {
+    double2 PUn, PUs, PVn, PVs, ZUn, ZUs, ZVn, ZVs, Kn, Ks;
+    get_pair(rings + 2 * RS, P, r, PUn, PUs);
+    get_pair(rings + 3 * RS, P, r, PVn, PVs);
+    get_pair(rings + 4 * RS, P, r, ZUn, ZUs);
+    get_pair(rings + 5 * RS, P, r, ZVn, ZVs);
+    get_pair(rings + 6 * RS, P, r, Kn, Ks);
+    const double rwa = r * wc * ia, wa = wc * ia;
+    // P-vectors: phi, zeta, delta, ke ; H-vectors: phi, zeta, delta
+    put_x(xm, xl, 0, r, jh, ir_scale(PUn, -rwa), ir_scale(PUs, -rwa), eq);
+    put_x(xm, xl, 1, r, jh, cadd2(cscale(A1n, w), ir_scale(ZUn, -rwa)),
+          cadd2(cscale(A1s, w), ir_scale(ZUs, -rwa)), eq);
+    put_x(xm, xl, 2, r, jh, cadd2(cscale(A2n, w), ir_scale(ZVn, rwa)),
+          cadd2(cscale(A2s, w), ir_scale(ZVs, rwa)), eq);
+    put_x(xm, xl, 3, r, jh, cscale(Kn, w), cscale(Ks, w), eq);
+    put_x(xm, xl, 4, r, jh, cscale(PVn, wa), cscale(PVs, wa), eq);
+    put_x(xm, xl, 5, r, jh, cscale(ZVn, wa), cscale(ZVs, wa), eq);
+    put_x(xm, xl, 6, r, jh, cscale(ZUn, wa), cscale(ZUs, wa), eq);
+  }
+}
+
 template <bool NONLIN>
 __device__ __forceinline__ void swe_grid_output(const double2* rings, const PlanDev& P, double* xm,
                                                 const XLayout& xl, int jh, double w, double wc,
                                                 double ia) {
-  const int RS = P.ring_stride;
   const bool eq = (jn_of(P, jh) == js_of(P, jh));
-  for (int r = threadIdx.x; r <= P.R; r += blockDim.x) {
-    double2 A1n, A1s, A2n, A2s;
-    get_pair(rings, P, r, A1n, A1s);
-    get_pair(rings + RS, P, r, A2n, A2s);
-    if (!NONLIN) {
-      put_x(xm, xl, 0, r, jh, cscale(A1n, w), cscale(A1s, w), eq);
-      put_x(xm, xl, 1, r, jh, cscale(A2n, w), cscale(A2s, w), eq);
-    } else {
-      double2 PUn, PUs, PVn, PVs, ZUn, ZUs, ZVn, ZVs, Kn, Ks;
-      get_pair(rings + 2 * RS, P, r, PUn, PUs);
-      get_pair(rings + 3 * RS, P, r, PVn, PVs);
-      get_pair(rings + 4 * RS, P, r, ZUn, ZUs);
-      get_pair(rings + 5 * RS, P, r, ZVn, ZVs);
-      get_pair(rings + 6 * RS, P, r, Kn, Ks);
-      const double rwa = r * wc * ia, wa = wc * ia;
-      // P-vectors: phi, zeta, delta, ke ; H-vectors: phi, zeta, delta
-      put_x(xm, xl, 0, r, jh, ir_scale(PUn, -rwa), ir_scale(PUs, -rwa), eq);
-      put_x(xm, xl, 1, r, jh, cadd2(cscale(A1n, w), ir_scale(ZUn, -rwa)),
-            cadd2(cscale(A1s, w), ir_scale(ZUs, -rwa)), eq);
-      put_x(xm, xl, 2, r, jh, cadd2(cscale(A2n, w), ir_scale(ZVn, rwa)),
-            cadd2(cscale(A2s, w), ir_scale(ZVs, rwa)), eq);
-      put_x(xm, xl, 3, r, jh, cscale(Kn, w), cscale(Ks, w), eq);
-      put_x(xm, xl, 4, r, jh, cscale(PVn, wa), cscale(PVs, wa), eq);
-      put_x(xm, xl, 5, r, jh, cscale(ZVn, wa), cscale(ZVs, wa), eq);
-      put_x(xm, xl, 6, r, jh, cscale(ZUn, wa), cscale(ZUs, wa), eq);
-    }
-  }
+  for (int r = threadIdx.x; r <= P.R; r += blockDim.x)
+    swe_out_one<NONLIN>(rings, P, xm, xl, r, jh, w, wc, ia, eq);
 }
 
 // Fused SWE grid stage with register FFTs (n_lon = 32 K), one latitude pair per
@@ -500,7 +510,15 @@ __device__ __forceinline__ void swe_grid_output(const double2* rings, const Plan
 // register staging), and warp w transforms rings w, w + nwarps, ...
 // K >= 16: 6 warps (5 inverse FFTs in one round) at <= 170 registers so two
 // CTAs share an SM; smaller rings: 8 warps.
-template <int K, bool NONLIN>
+//
+// CL: the CTA is one of a cluster of 4 covering one 4-latitude block of x.
+// After the forward FFTs the cluster synchronises and CTA c computes the
+// vectors of wavenumbers [c (R+1)/4, (c+1)(R+1)/4) for all 4 latitude pairs,
+// reading the other CTAs' spectra through distributed shared memory, so 4
+// consecutive threads write each 32-byte x sector whole (one pair per CTA
+// would write 8-byte quarters of it); a second cluster barrier keeps every
+// CTA's rings alive until the others have read them.
+template <int K, bool NONLIN, bool CL = false>
 __global__ void __launch_bounds__((K) >= 16 ? 192 : 256, 2) swe_grid_reg_kernel(PlanDev P, const double2* eo,
                                                         long long eo_mstride, double* x,
                                                         XLayout xl, double omega, double radius,
@@ -568,8 +586,27 @@ __global__ void __launch_bounds__((K) >= 16 ? 192 : 256, 2) swe_grid_reg_kernel(
     }
   }
   __syncthreads();
-  const double w = P.w_n[jh];
-  swe_grid_output<NONLIN>(rings, P, x + (size_t)m * xl.mstride, xl, jh, w, w * ic2, 1.0 / radius);
+  if constexpr (!CL) {
+    const double w = P.w_n[jh];
+    swe_grid_output<NONLIN>(rings, P, x + (size_t)m * xl.mstride, xl, jh, w, w * ic2, 1.0 / radius);
+  } else {
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const int c = (int)cl.block_rank();
+    const int jb0 = jh - c;                  // first latitude pair of this cluster's block
+    const int nr = P.R + 1, r_lo = c * nr / 4, r_hi = (c + 1) * nr / 4;
+    double* xm = x + (size_t)m * xl.mstride;
+    const double ia = 1.0 / radius;
+    for (int idx = threadIdx.x; idx < (r_hi - r_lo) * 4; idx += blockDim.x) {
+      const int i = idx & 3, r = r_lo + (idx >> 2);
+      const int jhi = jb0 + i;
+      const double mui = P.mu_n[jhi], wi = P.w_n[jhi];
+      const double2* ri = cl.map_shared_rank(rings, i);
+      swe_out_one<NONLIN>(ri, P, xm, xl, r, jhi, wi, wi / (1.0 - mui * mui), ia,
+                          jn_of(P, jhi) == js_of(P, jhi));
+    }
+    cl.sync();
+  }
 }
 
 // Split SWE grid stage, second kernel (register FFTs): the 5 grids come from
@@ -998,9 +1035,20 @@ int swe_reg_launch(const PlanDev& P, const double2* eo, long long eo_mstride, do
   const size_t smem = sizeof(double2) * nr * P.ring_stride;
   dim3 gridDim(jh_end - jh_begin, nmembers);
   if (gridDim.x == 0) return kOk;
+  static const int cl_knob = env_int("SWSDC_SWE_CLUSTER", 1);
+  const bool cl = cl_knob && (jh_begin % 4 == 0) && ((jh_end - jh_begin) % 4 == 0);
+  const int threads = K >= 16 ? 192 : 256;
+  if (cl) {
+    SW_TRY(set_smem((const void*)swe_grid_reg_kernel<K, NONLIN, true>, smem));
+    StageScope sc("swe_grid", st);
+    SW_CUDA(launch_pdl_cluster(swe_grid_reg_kernel<K, NONLIN, true>, dim3(gridDim), dim3(threads),
+                               smem, st, 4, P, eo, eo_mstride, x, xl, omega, radius, jh_begin));
+    SW_LAUNCH_CHECK();
+    return kOk;
+  }
   SW_TRY(set_smem((const void*)swe_grid_reg_kernel<K, NONLIN>, smem));
   StageScope sc("swe_grid", st);
-  SW_CUDA(launch_pdl(swe_grid_reg_kernel<K, NONLIN>, dim3(gridDim), dim3(K >= 16 ? 192 : 256), smem, st, P, eo, eo_mstride, x, xl, omega, radius, jh_begin));
+  SW_CUDA(launch_pdl(swe_grid_reg_kernel<K, NONLIN>, dim3(gridDim), dim3(threads), smem, st, P, eo, eo_mstride, x, xl, omega, radius, jh_begin));
   SW_LAUNCH_CHECK();
   return kOk;
 }
