@@ -299,7 +299,7 @@ syn_kernel(PlanDev P, SynArgs a) {
         __syncwarp();
         if (ci + 1 < c1) load_chunk<B, MODE>(nx, P, a, r, ci + 1, nstep, lane, jh, off_r);
         const int kn = min(kChunk, nstep - ci * kChunk);
-#pragma unroll 2
+#pragma unroll 4   // measured: 2 -> 4 saves 4.5%, 8 is slower
         for (int kk = 0; kk < kn; kk += 2) {
 #pragma unroll
           for (int b = 0; b < B; ++b) {
