@@ -105,6 +105,14 @@ int swsdc_combine(int n, const double* const* x, const double* w, long long coun
  * Lagrange rows, mlsdc.py:90-95) and the FAS combination (mlsdc.py:113-124) in one launch. */
 int swsdc_spec_combine(int n, const double* const* x, const double* w, const int* r_in, int r_out,
                        long long nmat, double* out, void* stream);
+/* nout (<= 16) independent spec_combine sums in one launch: output o takes the next
+ * nterms[o] entries of x / w / r_in (<= 96 terms in total); outputs may update one of
+ * their own inputs in place (Step D of mlsdc_iteration, mlsdc.py:226-238), but no
+ * output may be another output's input.  Used for the restriction, FAS and
+ * interpolation groups of an MLSDC iteration (mlsdc.py:83-124). */
+int swsdc_spec_combine_multi(int nout, const int* nterms, const double* const* x, const double* w,
+                             const int* r_in, int r_out, long long nmat, double* const* outs,
+                             void* stream);
 /* One SDC node update (sdc.py:196-206): b = sum_k w[k] x[k] (states at truncation R),
  * theta = solve_implicit(b, beta) (implicit.py:31-49), f_i = eval_f_i(theta)
  * (swe.py:206-217), for `batch` states.  Same status rules as swsdc_solve_implicit. */

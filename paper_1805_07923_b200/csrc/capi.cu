@@ -780,6 +780,36 @@ int swsdc_spec_combine(int n, const double* const* x, const double* w, const int
   return launch_spec_combine(a, nmat, S(stream));
 }
 
+int swsdc_spec_combine_multi(int nout, const int* nterms, const double* const* x, const double* w,
+                             const int* r_in, int r_out, long long nmat, double* const* outs,
+                             void* stream) {
+  if (nout < 0 || nout > kMultiOut || nmat < 0 || nmat > 65535 || r_out < 0) {
+    set_error("spec_combine_multi takes 0..16 outputs and <= 65535 matrices");
+    return kUsage;
+  }
+  MultiCombineArgs a{};
+  a.nout = nout;
+  a.rout = r_out;
+  int k = 0;
+  a.off[0] = 0;
+  for (int o = 0; o < nout; ++o) {
+    if (nterms[o] < 0 || k + nterms[o] > kMultiTerms) {
+      set_error("spec_combine_multi takes at most 96 terms in total");
+      return kUsage;
+    }
+    for (int t = 0; t < nterms[o]; ++t, ++k) {
+      if (r_in[k] < 0) { set_error("bad input truncation"); return kUsage; }
+      a.x[k] = reinterpret_cast<const double2*>(x[k]);
+      a.w[k] = w[k];
+      a.rin[k] = r_in[k];
+    }
+    a.off[o + 1] = k;
+    a.out[o] = reinterpret_cast<double2*>(outs[o]);
+  }
+  if (nmat == 0 || nout == 0) return kOk;
+  return launch_spec_combine_multi(a, (int)nmat, S(stream));
+}
+
 int swsdc_sweep_node(int R, const swsdc_params* q, double beta, int n, const double* const* x,
                      const double* w, int batch, double* theta, double* f_i, void* stream) {
   SW_TRY(check_params(q));

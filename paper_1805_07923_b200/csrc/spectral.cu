@@ -254,6 +254,30 @@ __global__ void __launch_bounds__(256) download_triangle_kernel(const double2* _
   }
 }
 
+// Grid (s blocks, r_out + 1 rows, nout * nmat): one row (m, r) of one output
+// per y/z coordinate, degrees s across x -- no per-element division.
+__global__ void __launch_bounds__(256) spec_combine_multi_kernel(MultiCombineArgs a, int nmat,
+                                                                 RowFilter rf) {
+  pdl_wait();
+  pdl_trigger();
+  const int r = blockIdx.y;
+  if (r % rf.mod != rf.rank) return;
+  const int o = blockIdx.z / nmat, m = blockIdx.z - o * nmat;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ro = a.rout;
+  if (s > ro) return;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int k = a.off[o]; k < a.off[o + 1]; ++k) {
+    const int ri = a.rin[k];
+    if (r <= ri && s <= ri) {
+      const double2 v = a.x[k][((size_t)m * (ri + 1) + r) * (ri + 1) + s];
+      acc.x = fma(a.w[k], v.x, acc.x);
+      acc.y = fma(a.w[k], v.y, acc.y);
+    }
+  }
+  a.out[o][((size_t)m * (ro + 1) + r) * (ro + 1) + s] = acc;
+}
+
 __global__ void spec_combine_kernel(SpecCombineArgs a, long long nmat, RowFilter rf) {
   pdl_wait();
   pdl_trigger();
@@ -375,7 +399,33 @@ int launch_combine(const CombineArgs& a, long long count, cudaStream_t st) {
   return kOk;
 }
 
+int launch_spec_combine_multi(const MultiCombineArgs& a, int nmat, cudaStream_t st) {
+  if (a.nout <= 0 || nmat <= 0) return kOk;
+  const int row = a.rout + 1;
+  const int threads = row >= 256 ? 256 : ((row + 31) / 32) * 32;
+  const long long z = (long long)a.nout * nmat;
+  if (z > 65535) {
+    set_error("spec_combine_multi: outputs x matrices exceed one launch");
+    return kUsage;
+  }
+  StageScope sc("spec_combine", st);
+  SW_CUDA(launch_pdl(spec_combine_multi_kernel, dim3((row + threads - 1) / threads, row, (unsigned)z),
+                     dim3(threads), 0, st, a, nmat, current_row_filter()));
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
 int launch_spec_combine(const SpecCombineArgs& a, long long nmat, cudaStream_t st) {
+  if ((long long)nmat <= 65535) {   // one output of the division-free multi kernel
+    MultiCombineArgs m{};
+    for (int k = 0; k < a.n; ++k) { m.x[k] = a.x[k]; m.w[k] = a.w[k]; m.rin[k] = a.rin[k]; }
+    m.off[0] = 0;
+    m.off[1] = a.n;
+    m.out[0] = a.out;
+    m.nout = 1;
+    m.rout = a.rout;
+    return launch_spec_combine_multi(m, (int)nmat, st);
+  }
   const long long n = nmat * (a.rout + 1) * (a.rout + 1);
   StageScope sc("spec_combine", st);
   SW_CUDA(launch_pdl(spec_combine_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, a, nmat, current_row_filter()));

@@ -45,6 +45,20 @@ struct SpecCombineArgs {
   int rout;
 };
 int launch_spec_combine(const SpecCombineArgs& a, long long nmat, cudaStream_t st);
+// Several independent weighted sums in one launch: output o (< nout) is
+// sum over terms [off[o], off[o+1]) of w_k * resize(x_k, rin_k -> rout).
+constexpr int kMultiOut = 16;
+constexpr int kMultiTerms = 96;
+struct MultiCombineArgs {
+  const double2* x[kMultiTerms];
+  double w[kMultiTerms];
+  int rin[kMultiTerms];
+  int off[kMultiOut + 1];
+  double2* out[kMultiOut];
+  int nout;
+  int rout;
+};
+int launch_spec_combine_multi(const MultiCombineArgs& a, int nmat, cudaStream_t st);
 // One sweep node (sdc.py:196-206 fused): b = sum_k w_k x_k (all at R);
 // theta = solve(b, beta); fi = L_G(theta).  nstates = states per input.
 int launch_sweep_node(int R, const ModelConsts& c, double beta, const SpecCombineArgs& a,

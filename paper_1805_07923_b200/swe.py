@@ -95,6 +95,53 @@ def spec_combine(weights, tensors, r_out: int, out: torch.Tensor | None = None) 
     return out
 
 
+def spec_combine_multi(jobs, r_out: int) -> list:
+    """Several independent spec_combine sums [(weights, tensors, out or None), ...]
+    in as few launches as the kernel's limits allow (16 outputs, 96 terms).
+    Outputs may update one of their own inputs in place; no output may be
+    another job's input.  Returns the output tensors in job order."""
+    outs, batch = [], []
+    prep = []
+    for weights, tensors, out in jobs:
+        pairs = [(float(w), t) for w, t in zip(weights, tensors) if float(w) != 0.0]
+        ref = tensors[0]
+        lead = tuple(ref.shape[:-2])
+        if any(tuple(t.shape[:-2]) != lead for t in tensors):
+            raise ValueError("spec_combine needs one leading shape")
+        if out is None:
+            out = torch.empty(lead + (r_out + 1, r_out + 1), dtype=torch.complex128,
+                              device=ref.device)
+        if len(pairs) > 32:
+            raise ValueError("spec_combine supports at most 32 weighted terms")
+        prep.append((pairs, out, lead))
+        outs.append(out)
+    if not prep:
+        return outs
+    lead0 = prep[0][2]
+    if any(p[2] != lead0 for p in prep):
+        raise ValueError("spec_combine_multi needs one leading shape across jobs")
+    nmat = math.prod(lead0)
+    dev = prep[0][1].device
+    i = 0
+    while i < len(prep):
+        # greedy chunk within the kernel's limits
+        group, terms = [], 0
+        while i < len(prep) and len(group) < 16 and terms + len(prep[i][0]) <= 96:
+            group.append(prep[i])
+            terms += len(prep[i][0])
+            i += 1
+        nt = (ctypes.c_int * len(group))(*[len(p[0]) for p in group])
+        flat = [pt for p in group for pt in p[0]]
+        ptrs = (ctypes.c_void_p * max(1, len(flat)))(*[t.data_ptr() for _, t in flat])
+        ws = (ctypes.c_double * max(1, len(flat)))(*[w for w, _ in flat])
+        rin = (ctypes.c_int * max(1, len(flat)))(*[t.shape[-1] - 1 for _, t in flat])
+        outp = (ctypes.c_void_p * len(group))(*[p[1].data_ptr() for p in group])
+        with _dev_guard(dev):
+            _lib.check(_lib.load().swsdc_spec_combine_multi(len(group), nt, ptrs, ws, rin, r_out,
+                                                            nmat, outp, _stream_ptr(dev)))
+    return outs
+
+
 class PrognosticState:
     """Spectral state (phi_prime, zeta, delta) at one truncation (swe.py:44-125)."""
 

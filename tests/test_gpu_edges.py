@@ -130,3 +130,25 @@ def test_usage_and_numerical_errors():
         rhs.solve_implicit(st, -1.0)                                        # beta < 0
     with pytest.raises(ValueError):
         swe.ModelParams(**{**TEST_PARAMS, "h_bar": -1.0})                  # non-physical depth
+
+
+def test_spec_combine_multi_equals_single_launches():
+    """The batched restriction/FAS/interpolation launches give bitwise the same
+    sums as one spec_combine per output (same terms, same order), including
+    in-place outputs and mixed input truncations."""
+    from paper_1805_07923_b200 import swe
+    rng = np.random.default_rng(3)
+    dev = torch.device("cuda")
+    xs = [torch.as_tensor(_rand_coeffs(rng, R, 3), device=dev) for R in (21, 10, 21, 15)]
+    jobs = [([1.0, -0.5, 0.25], [xs[0], xs[1], xs[3]], None),
+            ([2.0, 1.0], [xs[3], xs[2]], None),
+            ([1.0, 0.5, -0.5], [xs[2].clone(), xs[0], xs[1]], None)]
+    jobs[2] = (jobs[2][0], jobs[2][1], jobs[2][1][0])          # in place on its own input
+    want = [swe.spec_combine(w, [t.clone() for t in x], 21) for w, x, _ in jobs]
+    got = swe.spec_combine_multi(jobs, 21)
+    for g, w in zip(got, want):
+        assert torch.equal(g, w)
+    many = [([1.0, 1.0], [xs[0], xs[2]], None) for _ in range(40)]   # > 16 outputs: chunked
+    outs = swe.spec_combine_multi(many, 15)
+    ref = swe.spec_combine([1.0, 1.0], [xs[0], xs[2]], 15)
+    assert all(torch.equal(o, ref) for o in outs)
