@@ -33,8 +33,14 @@ print('stalls / pipes:', names)
 for i, col in enumerate(h):
     if col in keys or ('pcsamp_warps_issue_stalled' in col and not col.endswith('not_issued')):
         try:
-            vals = [float(r[i]) for r in rows[2:]]
+            vals = [float(r[i].replace(',', '')) for r in rows[2:]]
         except ValueError:
             continue
+        unit = rows[1][i]
+        # ncu picks byte units per metric; report bytes in MB so columns compare
+        scale = {'byte': 1e-6, 'Kbyte': 1e-3, 'Mbyte': 1.0, 'Gbyte': 1e3}.get(unit)
+        if scale is not None:
+            vals = [v * scale for v in vals]
+            unit = 'MB'
         if max(vals) > 0.5 or col in keys:
-            print('  ', col[-58:].ljust(58), ' '.join(f'{v:11.2f}' for v in vals))
+            print('  ', (col[-52:] + f' [{unit}]').ljust(60), ' '.join(f'{v:11.2f}' for v in vals))
