@@ -517,7 +517,7 @@ def run_mlsdc(name, cfg, world, rank, dev, dist, flush_l2, peak_fp64):
         ev[k][1].record()
     torch.cuda.synchronize()
     launches = _lib.launch_count() - l0
-    finite = bool(stp._g.flag.item())
+    finite = int(stp._g.bad.item()) == 0
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
     t_ms = max_over_ranks(t_ms, dist, dev)
     total_members = mine * world if members >= world else members

@@ -113,6 +113,9 @@ int swsdc_spec_combine(int n, const double* const* x, const double* w, const int
 int swsdc_spec_combine_multi(int nout, const int* nterms, const double* const* x, const double* w,
                              const int* r_in, int r_out, long long nmat, double* const* outs,
                              void* stream);
+/* dst = src over n doubles and *bad = (any value non-finite): the stepper's per-step state
+ * copy and finiteness check (harness.py:257) in one pass; *bad is cleared first. */
+int swsdc_copy_finite(const double* src, double* dst, long long n, int* bad, void* stream);
 /* One SDC node update (sdc.py:196-206): b = sum_k w[k] x[k] (states at truncation R),
  * theta = solve_implicit(b, beta) (implicit.py:31-49), f_i = eval_f_i(theta)
  * (swe.py:206-217), for `batch` states.  Same status rules as swsdc_solve_implicit. */

@@ -780,6 +780,11 @@ int swsdc_spec_combine(int n, const double* const* x, const double* w, const int
   return launch_spec_combine(a, nmat, S(stream));
 }
 
+int swsdc_copy_finite(const double* src, double* dst, long long n, int* bad, void* stream) {
+  if (n < 0 || !bad) { set_error("bad copy_finite arguments"); return kUsage; }
+  return launch_copy_finite(src, dst, n, bad, S(stream));
+}
+
 int swsdc_spec_combine_multi(int nout, const int* nterms, const double* const* x, const double* w,
                              const int* r_in, int r_out, long long nmat, double* const* outs,
                              void* stream) {

@@ -479,6 +479,37 @@ __global__ void zero_lower_kernel(double2* out, int R, long long nmat) {
   }
 }
 
+// dst = src over n doubles; *bad = 1 if any value is not finite (*bad is
+// cleared by the caller first): the graph stepper's state copy and per-step
+// finiteness check (harness.py:257) in one pass.
+__global__ void __launch_bounds__(256) copy_finite_kernel(const double* __restrict__ src,
+                                                          double* __restrict__ dst, long long n,
+                                                          int* bad) {
+  pdl_wait();
+  pdl_trigger();
+  bool ok = true;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v = src[i];
+    dst[i] = v;
+    ok = ok && isfinite(v);
+  }
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicExch(bad, 1);
+}
+
+int launch_copy_finite(const double* src, double* dst, long long n, int* bad, cudaStream_t st) {
+  SW_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  if (n <= 0) return kOk;
+  StageScope sc("copy_finite", st);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const long long want = (n + 255) / 256;
+  const int blocks = (int)std::min<long long>(want, 4LL * sms);
+  SW_CUDA(launch_pdl(copy_finite_kernel, dim3(blocks), dim3(256), 0, st, src, dst, n, bad));
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
 int launch_zero_lower(double2* out, int R, long long nmat, cudaStream_t st) {
   const long long n = nmat * (R + 1) * (R + 1);
   StageScope sc("zero_lower", st);

@@ -67,6 +67,7 @@ int launch_upload_triangle(const double2* host, double2* out, int R, long long n
                            cudaStream_t st);
 int launch_download_triangle(const double2* dev, double2* host, int R, long long nmat,
                              int write_lower, cudaStream_t st);
+int launch_copy_finite(const double* src, double* dst, long long n, int* bad, cudaStream_t st);
 int launch_zero_lower(double2* out, int R, long long nmat, cudaStream_t st);
 int launch_resize(const double2* in, int rin, double2* out, int rout, long long nmat,
                   cudaStream_t st);

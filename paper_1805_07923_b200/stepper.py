@@ -17,7 +17,8 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import mlsdc, sdc
+from . import _lib, mlsdc, sdc
+from .spharm import _dev_guard, _ptr, _stream_ptr
 from .swe import EvalCounters, PrognosticState
 
 
@@ -42,7 +43,9 @@ class _GraphStep:
         self.x = x_static
         self.body = body
         self.levels = levels
-        self.flag = torch.ones((), dtype=torch.bool, device=x_static.device)
+        # device int: 1 if the last step produced a non-finite value (written by
+        # the library's fused copy + finiteness kernel inside the graph)
+        self.bad = torch.zeros((), dtype=torch.int32, device=x_static.device)
         self.graph = None
         # eager warm-up on a side stream: sizes every plan workspace and sets
         # kernel attributes before capture (nothing may allocate in capture)
@@ -68,8 +71,11 @@ class _GraphStep:
 
     def _step(self):
         y = self.body(self.x)
-        self.x.copy_(y)
-        torch.all(torch.isfinite(torch.view_as_real(self.x)), out=self.flag)
+        dev = self.x.device
+        with _dev_guard(dev):
+            _lib.check(_lib.load().swsdc_copy_finite(
+                _ptr(y.contiguous()), _ptr(self.x), self.x.numel() * 2, _ptr(self.bad),
+                _stream_ptr(dev)))
 
     def replay(self):
         if self.graph is not None:
@@ -118,11 +124,11 @@ class MLSDCStepper:
 
     def run(self, n_steps: int) -> PrognosticState:
         """Advance n_steps; raise InstabilityError for the first non-finite step."""
-        flags = torch.empty(n_steps, dtype=torch.bool, device=self._g.x.device)
+        flags = torch.empty(n_steps, dtype=torch.int32, device=self._g.x.device)
         for k in range(n_steps):
             self._g.replay()
-            flags[k].copy_(self._g.flag)
-        bad = torch.nonzero(~flags)
+            flags[k].copy_(self._g.bad)
+        bad = torch.nonzero(flags)
         if bad.numel():
             raise InstabilityError(int(bad[0]))
         return self.state
@@ -157,11 +163,11 @@ class SDCStepper:
         return PrognosticState.from_tensor(self._g.x)
 
     def run(self, n_steps: int) -> PrognosticState:
-        flags = torch.empty(n_steps, dtype=torch.bool, device=self._g.x.device)
+        flags = torch.empty(n_steps, dtype=torch.int32, device=self._g.x.device)
         for k in range(n_steps):
             self._g.replay()
-            flags[k].copy_(self._g.flag)
-        bad = torch.nonzero(~flags)
+            flags[k].copy_(self._g.bad)
+        bad = torch.nonzero(flags)
         if bad.numel():
             raise InstabilityError(int(bad[0]))
         return self.state
