@@ -1133,9 +1133,12 @@ bool swe_grid_fits(const PlanDev& P) {
 
 // Small batches (few latitude pairs x members) leave the one-pair-per-CTA fused
 // kernel short of CTAs; the split path (f2g of the 5 grids, then the role-split
-// forward kernel) runs ~3x more warps.  SWSDC_SWE_SPLIT: 0 never, 2 always.
+// forward kernel) runs ~3x more warps.  SWSDC_SWE_SPLIT: 0 never (default),
+// 1 below SMs/2 pairs x members, 2 always.
 bool swe_split_preferred(const PlanDev& P, long long pair_members) {
-  static const int knob = env_int("SWSDC_SWE_SPLIT", 1);
+  // default off: with the cluster output and PDL the fused kernel is as fast
+  // even for config 0's tiny grids (0.266 vs 0.268 ms/step, same-box A/B)
+  static const int knob = env_int("SWSDC_SWE_SPLIT", 0);
   if (knob == 0 || !use_reg_fft(P)) return false;
   if (knob == 2) return true;
   static int sms = 0;
