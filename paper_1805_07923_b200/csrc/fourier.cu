@@ -519,7 +519,7 @@ __device__ __forceinline__ void swe_grid_output(const double2* rings, const Plan
 // would write 8-byte quarters of it); a second cluster barrier keeps every
 // CTA's rings alive until the others have read them.
 template <int K, bool NONLIN, bool CL = false>
-__global__ void __launch_bounds__((K) >= 16 ? 192 : 256, 2) swe_grid_reg_kernel(PlanDev P, const double2* eo,
+__global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) swe_grid_reg_kernel(PlanDev P, const double2* eo,
                                                         long long eo_mstride, double* x,
                                                         XLayout xl, double omega, double radius,
                                                         int jh_begin) {
@@ -1037,7 +1037,8 @@ int swe_reg_launch(const PlanDev& P, const double2* eo, long long eo_mstride, do
   if (gridDim.x == 0) return kOk;
   static const int cl_knob = env_int("SWSDC_SWE_CLUSTER", 1);
   const bool cl = cl_knob && (jh_begin % 4 == 0) && ((jh_end - jh_begin) % 4 == 0);
-  const int threads = K >= 16 ? 192 : 256;
+  // warps: 6 for K >= 20 (registers), 7 for K = 16 (all forward FFTs in one round), 8 below
+  const int threads = K >= 20 ? 192 : K == 16 ? 224 : 256;
   if (cl) {
     SW_TRY(set_smem((const void*)swe_grid_reg_kernel<K, NONLIN, true>, smem));
     StageScope sc("swe_grid", st);
