@@ -109,10 +109,12 @@ int swsdc_spec_combine(int n, const double* const* x, const double* w, const int
  * nterms[o] entries of x / w / r_in (<= 96 terms in total); outputs may update one of
  * their own inputs in place (Step D of mlsdc_iteration, mlsdc.py:226-238), but no
  * output may be another output's input.  Used for the restriction, FAS and
- * interpolation groups of an MLSDC iteration (mlsdc.py:83-124). */
+ * interpolation groups of an MLSDC iteration (mlsdc.py:83-124).  ext (nullable): per output,
+ * rows and columns above ext[o] are left untouched -- for in-place outputs whose other terms
+ * are all at truncation <= ext[o] (x += padded coarse correction), only that block changes. */
 int swsdc_spec_combine_multi(int nout, const int* nterms, const double* const* x, const double* w,
                              const int* r_in, int r_out, long long nmat, double* const* outs,
-                             void* stream);
+                             const int* ext, void* stream);
 /* dst = src over n doubles and *bad = (any value non-finite): the stepper's per-step state
  * copy and finiteness check (harness.py:257) in one pass; *bad is cleared first. */
 int swsdc_copy_finite(const double* src, double* dst, long long n, int* bad, void* stream);

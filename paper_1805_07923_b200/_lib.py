@@ -55,7 +55,7 @@ _SIGNATURES = {
     "swsdc_combine": ([_I, ctypes.POINTER(_P), ctypes.POINTER(_D), _LL, _P, _P], _I),
     "swsdc_resize": ([_P, _I, _P, _I, _LL, _P], _I),
     "swsdc_upload_coeffs": ([_P, _I, _LL, _P, _P], _I),
-    "swsdc_spec_combine_multi": ([_I, _P, _P, _P, _P, _I, _LL, _P, _P], _I),
+    "swsdc_spec_combine_multi": ([_I, _P, _P, _P, _P, _I, _LL, _P, _P, _P], _I),
     "swsdc_copy_finite": ([_P, _P, _LL, _P, _P], _I),
     "swsdc_download_coeffs": ([_P, _I, _LL, _P, _I, _P], _I),
     "swsdc_spec_combine": ([_I, ctypes.POINTER(_P), ctypes.POINTER(_D), ctypes.POINTER(_I), _I, _LL,

@@ -787,7 +787,7 @@ int swsdc_copy_finite(const double* src, double* dst, long long n, int* bad, voi
 
 int swsdc_spec_combine_multi(int nout, const int* nterms, const double* const* x, const double* w,
                              const int* r_in, int r_out, long long nmat, double* const* outs,
-                             void* stream) {
+                             const int* ext, void* stream) {
   if (nout < 0 || nout > kMultiOut || nmat < 0 || nmat > 65535 || r_out < 0) {
     set_error("spec_combine_multi takes 0..16 outputs and <= 65535 matrices");
     return kUsage;
@@ -810,6 +810,7 @@ int swsdc_spec_combine_multi(int nout, const int* nterms, const double* const* x
     }
     a.off[o + 1] = k;
     a.out[o] = reinterpret_cast<double2*>(outs[o]);
+    a.ext[o] = (ext && ext[o] >= 0 && ext[o] < r_out) ? ext[o] : r_out;
   }
   if (nmat == 0 || nout == 0) return kOk;
   return launch_spec_combine_multi(a, (int)nmat, S(stream));

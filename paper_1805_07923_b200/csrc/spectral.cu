@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(256) spec_combine_multi_kernel(MultiCombineArg
   const int o = blockIdx.z / nmat, m = blockIdx.z - o * nmat;
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   const int ro = a.rout;
-  if (s > ro) return;
+  if (r > a.ext[o] || s > a.ext[o]) return;
   double2 acc = make_double2(0.0, 0.0);
   for (int k = a.off[o]; k < a.off[o + 1]; ++k) {
     const int ri = a.rin[k];
@@ -422,6 +422,7 @@ int launch_spec_combine(const SpecCombineArgs& a, long long nmat, cudaStream_t s
     m.off[0] = 0;
     m.off[1] = a.n;
     m.out[0] = a.out;
+    m.ext[0] = a.rout;
     m.nout = 1;
     m.rout = a.rout;
     return launch_spec_combine_multi(m, (int)nmat, st);

@@ -55,6 +55,8 @@ struct MultiCombineArgs {
   int rin[kMultiTerms];
   int off[kMultiOut + 1];
   double2* out[kMultiOut];
+  int ext[kMultiOut];      // rows/columns > ext are left as they are (in-place outputs
+                           // whose other terms are all coarser: x += padded correction)
   int nout;
   int rout;
 };

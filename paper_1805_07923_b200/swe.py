@@ -113,7 +113,13 @@ def spec_combine_multi(jobs, r_out: int) -> list:
                               device=ref.device)
         if len(pairs) > 32:
             raise ValueError("spec_combine supports at most 32 weighted terms")
-        prep.append((pairs, out, lead))
+        # in place with a unit self term and only coarser other terms: entries
+        # beyond the other terms' truncation are unchanged, so skip them
+        ext = r_out
+        if pairs and pairs[0][1].data_ptr() == out.data_ptr() and pairs[0][0] == 1.0 \
+                and pairs[0][1].shape[-1] - 1 == r_out and len(pairs) > 1:
+            ext = max(t.shape[-1] - 1 for _, t in pairs[1:])
+        prep.append((pairs, out, lead, ext))
         outs.append(out)
     if not prep:
         return outs
@@ -136,9 +142,10 @@ def spec_combine_multi(jobs, r_out: int) -> list:
         ws = (ctypes.c_double * max(1, len(flat)))(*[w for w, _ in flat])
         rin = (ctypes.c_int * max(1, len(flat)))(*[t.shape[-1] - 1 for _, t in flat])
         outp = (ctypes.c_void_p * len(group))(*[p[1].data_ptr() for p in group])
+        exts = (ctypes.c_int * len(group))(*[p[3] for p in group])
         with _dev_guard(dev):
             _lib.check(_lib.load().swsdc_spec_combine_multi(len(group), nt, ptrs, ws, rin, r_out,
-                                                            nmat, outp, _stream_ptr(dev)))
+                                                            nmat, outp, exts, _stream_ptr(dev)))
     return outs
 
 
