@@ -273,8 +273,8 @@ int fe_grid_stage(swsdc_plan* p, bool nl, const double2* eo, int batch, double* 
                swe_split_preferred(P, (long long)(jh_end - jh_begin) * batch);
   const long long gfield = (long long)P.I * P.J;
   const bool reg = fourier_reg_fft(P);
-  // ring layout (register-FFT split): Jh x I complex per field; grid layout: I x J real
-  const size_t per_field = reg ? sizeof(double2) * (size_t)P.Jh * P.I : sizeof(double) * gfield;
+  // ring layout: Jh x I complex per field (>= I x J real for odd J)
+  const size_t per_field = std::max<size_t>(sizeof(double2) * (size_t)P.Jh * P.I, sizeof(double) * gfield);
   if (split) {
     bool ok = true;
     SW_TRY(grow_grid_ws(p, per_field * 5 * batch, st, &ok));
@@ -292,10 +292,12 @@ int fe_grid_stage(swsdc_plan* p, bool nl, const double2* eo, int batch, double* 
   if (reg)
     return launch_swe_split_reg(P, nl, eo, fstride, reinterpret_cast<double2*>(p->grid_ws), x, xl,
                                 batch, omega, radius, st, jh_begin, jh_end);
-  double* g = reinterpret_cast<double*>(p->grid_ws);
-  SW_TRY(launch_fourier_to_grid(P, eo, fstride, g, gfield, 5 * batch, st, jh_begin, jh_end));
-  return launch_swe_products(P, nl, g, gfield, 5 * gfield, x, xl, batch, omega, radius, st,
-                             jh_begin, jh_end);
+  // smem-FFT split path: grids travel in the ring layout (coalesced rows per pair)
+  double2* rg = reinterpret_cast<double2*>(p->grid_ws);
+  const long long rfield = (long long)P.Jh * P.I;
+  SW_TRY(launch_fourier_to_rings(P, eo, fstride, rg, rfield, 5 * batch, st, jh_begin, jh_end));
+  return launch_swe_products(P, nl, reinterpret_cast<const double*>(rg), rfield, 5 * rfield, x, xl,
+                             batch, omega, radius, st, jh_begin, jh_end);
 }
 
 // Legendre analysis of the nv vectors (XLayout xl) of each member into out.

@@ -172,7 +172,9 @@ __device__ __forceinline__ void put_x(double* x, const XLayout& L, int v, int r,
 // ---------------------------------------------------------------------------
 // (E, O) -> grid, np pairs per CTA.  grid: [f][I][J]
 // ---------------------------------------------------------------------------
-template <bool BIGP>
+// RINGS: write each pair's ring (north, south) contiguously, rings_out[f][jh][il]
+// (double2, grid_fstride in double2), the layout swe_prod_kernel reads coalesced.
+template <bool BIGP, bool RINGS = false>
 __global__ void __launch_bounds__(256, 2) f2g_kernel(PlanDev P, const double2* eo, long long eo_fstride, double* grid,
                            long long grid_fstride, int lnp, int jh_begin, int jh_end) {
   pdl_wait();
@@ -186,6 +188,15 @@ __global__ void __launch_bounds__(256, 2) f2g_kernel(PlanDev P, const double2* e
   fill_rings(rings, Q, eo + (size_t)f * eo_fstride, 0, 1, np, lnp, jh0);
   __syncthreads();
   fft_inverse<BIGP>(rings, np, P);
+  if (RINGS) {
+    double2* out = reinterpret_cast<double2*>(grid) + (size_t)f * grid_fstride;
+    for (int i = 0; i < np && jh0 + i < jh_end; ++i) {
+      const double2* ring = rings + (size_t)i * P.ring_stride;
+      double2* dst = out + (size_t)(jh0 + i) * P.I;
+      for (int il = threadIdx.x; il < P.I; il += blockDim.x) dst[il] = ring[swfft::pad_idx(il)];
+    }
+    return;
+  }
   double* g = grid + (size_t)f * grid_fstride;
   for (int idx = threadIdx.x; idx < (P.I << lnp); idx += blockDim.x) {
     const int il = idx >> lnp, i = idx & (np - 1);
@@ -605,7 +616,11 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
       swe_out_one<NONLIN>(ri, P, xm, xl, r, jhi, wi, wi / (1.0 - mui * mui), ia,
                           jn_of(P, jhi) == js_of(P, jhi));
     }
-    cl.sync();
+    // only the remote shared-memory reads above must be complete before a CTA
+    // may exit, and they are (their values were consumed): a relaxed arrive
+    // does not wait for this CTA's outstanding x stores as cl.sync()'s release would
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
   }
 }
 
@@ -818,7 +833,7 @@ __global__ void __launch_bounds__(256, 2) swe_grid_kernel(PlanDev P, const doubl
 // transformed pairwise through 2 rings, each pair completing its analysis
 // vectors: (A1, ZU) -> v1, v6; (A2, ZV) -> v2, v5; (PU, PV) -> v0, v4; KE -> v3.
 // ---------------------------------------------------------------------------
-template <bool NONLIN, bool BIGP>
+template <bool NONLIN, bool BIGP, bool RINGS = false>
 __global__ void __launch_bounds__(256, 1) swe_prod_kernel(PlanDev P, const double* grids,
                                                           long long gfield, long long gmember,
                                                           double* x, XLayout xl, double omega,
@@ -835,8 +850,11 @@ __global__ void __launch_bounds__(256, 1) swe_prod_kernel(PlanDev P, const doubl
   const double fn = 2.0 * omega * mu, c2o = 2.0 * omega / radius, ic2 = 1.0 / (1.0 - mu * mu);
   const double w = P.w_n[jh], wc = w * ic2, ia = 1.0 / radius;
   double* xm = x + (size_t)m * xl.mstride;
-  // grid value of field q at longitude il, north (x) and south (y)
+  // grid value of field q at longitude il, north (x) and south (y); RINGS:
+  // rings[m][q][jh][il] (double2; gfield, gmember in double2)
+  const double2* gr = reinterpret_cast<const double2*>(grids) + (size_t)m * gmember + (size_t)jh * I;
   auto gv = [&](int q, int il) {
+    if (RINGS) return gr[(size_t)q * gfield + il];
     const double* g = gm + (size_t)q * gfield + (size_t)il * P.J;
     return d2(g[jn], g[js]);
   };
@@ -978,16 +996,16 @@ int g2f_reg_launch(const PlanDev& P, const double* grid, const double* grid2,
     case 24: { constexpr int KK = 24; return CALL; }                              \
   }
 
-template <bool BIGP>
+template <bool BIGP, bool RINGS = false>
 int f2g_launch(const PlanDev& P, const double2* eo, long long eo_fstride, double* grid,
                long long grid_fstride, int nf, int jh_begin, int jh_end, cudaStream_t st) {
   const int lnp = pairs_log2(P, 1), np = 1 << lnp;
   const size_t smem = sizeof(double2) * np * P.ring_stride;
-  SW_TRY(set_smem((const void*)f2g_kernel<BIGP>, smem));
+  SW_TRY(set_smem((const void*)f2g_kernel<BIGP, RINGS>, smem));
   dim3 gridDim((jh_end - jh_begin + np - 1) / np, nf);
   if (gridDim.x == 0) return kOk;
   StageScope sc("fourier_to_grid", st);
-  SW_CUDA(launch_pdl(f2g_kernel<BIGP>, dim3(gridDim), dim3(pick_threads(np * max_butterflies(P), BIGP)), smem, st, P, eo, eo_fstride, grid, grid_fstride, lnp, jh_begin, jh_end));
+  SW_CUDA(launch_pdl(f2g_kernel<BIGP, RINGS>, dim3(gridDim), dim3(pick_threads(np * max_butterflies(P), BIGP)), smem, st, P, eo, eo_fstride, grid, grid_fstride, lnp, jh_begin, jh_end));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -1072,12 +1090,13 @@ template <bool NONLIN, bool BIGP>
 int swe_prod_launch(const PlanDev& P, const double* grids, long long gfield, long long gmember,
                     double* x, const XLayout& xl, int nmembers, double omega, double radius,
                     int jh_begin, int jh_end, cudaStream_t st) {
+  // grids in the ring layout (f2g_kernel<., true>): gfield / gmember in double2
   const size_t smem = sizeof(double2) * 2 * P.ring_stride;
-  SW_TRY(set_smem((const void*)swe_prod_kernel<NONLIN, BIGP>, smem));
+  SW_TRY(set_smem((const void*)swe_prod_kernel<NONLIN, BIGP, true>, smem));
   dim3 gridDim(jh_end - jh_begin, nmembers);
   if (gridDim.x == 0) return kOk;
   StageScope sc("swe_products", st);
-  SW_CUDA(launch_pdl(swe_prod_kernel<NONLIN, BIGP>, dim3(gridDim), dim3(BIGP ? 128 : 256), smem, st, P, grids, gfield, gmember, x, xl, omega, radius, jh_begin));
+  SW_CUDA(launch_pdl(swe_prod_kernel<NONLIN, BIGP, true>, dim3(gridDim), dim3(BIGP ? 128 : 256), smem, st, P, grids, gfield, gmember, x, xl, omega, radius, jh_begin));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -1165,6 +1184,18 @@ int launch_swe_products(const PlanDev& P, bool nonlinear, const double* grids, l
   }
   if (big) return swe_prod_launch<false, true>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
   return swe_prod_launch<false, false>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
+}
+
+// Smem-FFT inverse of nf (E, O) fields into the ring layout rings[f][jh][il]
+// (double2, ring_fstride in double2): the grid stage of the split F_E path.
+int launch_fourier_to_rings(const PlanDev& P, const double2* eo, long long eo_fstride,
+                            double2* rings, long long ring_fstride, int nf, cudaStream_t st,
+                            int jh_begin, int jh_end) {
+  if (jh_end < 0) jh_end = P.Jh;
+  double* g = reinterpret_cast<double*>(rings);
+  if (swfft::fft_needs_bigp(P.I))
+    return f2g_launch<true, true>(P, eo, eo_fstride, g, ring_fstride, nf, jh_begin, jh_end, st);
+  return f2g_launch<false, true>(P, eo, eo_fstride, g, ring_fstride, nf, jh_begin, jh_end, st);
 }
 
 int launch_fourier_to_grid(const PlanDev& P, const double2* eo, long long eo_fstride, double* grid,

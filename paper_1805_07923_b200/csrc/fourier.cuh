@@ -8,6 +8,11 @@ namespace swsdc {
 int launch_fourier_to_grid(const PlanDev& P, const double2* eo, long long eo_fstride, double* grid,
                            long long grid_fstride, int nf, cudaStream_t st, int jh_begin = 0,
                            int jh_end = -1);
+// (E, O) partial sums of nf fields -> rings [nf][Jh][I] (double2 north, south),
+// the grid layout of the split F_E path
+int launch_fourier_to_rings(const PlanDev& P, const double2* eo, long long eo_fstride,
+                            double2* rings, long long ring_fstride, int nf, cudaStream_t st,
+                            int jh_begin = 0, int jh_end = -1);
 // grids -> weighted (S, D) vectors in XLayout.  mode 0: plain (nf fields = nf
 // vectors of one member); mode 1: div/curl (nf (U, V) pairs = nf members of 4 vectors)
 int launch_grid_to_fourier(const PlanDev& P, int mode, const double* grid, const double* grid2,
@@ -25,8 +30,9 @@ bool fourier_reg_fft(const PlanDev& P);
 int launch_swe_split_reg(const PlanDev& P, bool nonlinear, const double2* eo, long long eo_fstride,
                          double2* ring_ws, double* x, const XLayout& xl, int nmembers,
                          double omega, double radius, cudaStream_t st, int jh_begin, int jh_end);
-// large-n_lon path: products + forward FFTs from 5 grids in HBM
-// (grids[m * gmember + q * gfield + il * J + j], q = U/a, V/a, zeta, delta, phi')
+// large-n_lon path: products + forward FFTs from 5 grids in HBM in the ring
+// layout (double2 rings[m * gmember + q * gfield + jh * I + il], q = U/a, V/a,
+// zeta, delta, phi'; strides in double2)
 int launch_swe_products(const PlanDev& P, bool nonlinear, const double* grids, long long gfield,
                         long long gmember, double* x, const XLayout& xl, int nmembers,
                         double omega, double radius, cudaStream_t st, int jh_begin = 0,
