@@ -1,5 +1,6 @@
 // C ABI (include/swsdc_b200.h): plan construction and the host-side
 // orchestration of the kernels for each reference entry point.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -25,7 +26,7 @@ struct swsdc_plan {
   PlanDev dev{};
   std::vector<void*> owned;
   // analysis work lists [smax = R, R + 1][lsplit = 1, 2]: CTAs of 4/lsplit chunks
-  int2* work[2][kAnaSplits] = {};      // [smax = R, R + 1][latitude split - 1]
+  int4* work[2][kAnaSplits] = {};      // [smax = R, R + 1][latitude split - 1]
   int nwork[2][kAnaSplits] = {};
   int nchunks[2] = {0, 0};
   int ldy = 0;
@@ -40,12 +41,12 @@ struct swsdc_plan {
     int mod = 1, rank = 0;
     int2* pairs = nullptr;
     int npairs = 0;
-    int2* work[2][kAnaSplits] = {};
+    int4* work[2][kAnaSplits] = {};
     int nwork[2][kAnaSplits] = {};
     int nchunks[2] = {0, 0};
   };
   std::vector<Shard> shards;
-  std::vector<std::vector<int2>> host_work[2];  // host copies of the analysis lists
+  std::vector<std::vector<int4>> host_work[2];  // host copies of the analysis lists
 };
 
 namespace swsdc {
@@ -191,13 +192,13 @@ const swsdc_plan::Shard* shard_for(swsdc_plan* p) {
   for (int i = 0; i < 2; ++i) {
     for (int r : rows) s.nchunks[i] += (R + i - r + 1 + kChunk - 1) / kChunk;
     for (int j = 0; j < kAnaSplits; ++j) {
-      std::vector<int2> w;
-      for (const int2& it : p->host_work[i][j])
+      std::vector<int4> w;
+      for (const int4& it : p->host_work[i][j])
         if (it.x % rf.mod == rf.rank) w.push_back(it);
       s.nwork[i][j] = (int)w.size();
       if (!w.empty()) {
-        if (cudaMalloc(&s.work[i][j], sizeof(int2) * w.size()) != cudaSuccess) return nullptr;
-        cudaMemcpy(s.work[i][j], w.data(), sizeof(int2) * w.size(), cudaMemcpyHostToDevice);
+        if (cudaMalloc(&s.work[i][j], sizeof(int4) * w.size()) != cudaSuccess) return nullptr;
+        cudaMemcpy(s.work[i][j], w.data(), sizeof(int4) * w.size(), cudaMemcpyHostToDevice);
         p->owned.push_back(s.work[i][j]);
       }
     }
@@ -206,7 +207,7 @@ const swsdc_plan::Shard* shard_for(swsdc_plan* p) {
   return &p->shards.back();
 }
 
-int upload_work(swsdc_plan* p, std::vector<int2> (&work)[2][kAnaSplits]) {
+int upload_work(swsdc_plan* p, std::vector<int4> (&work)[2][kAnaSplits]) {
   for (int i = 0; i < 2; ++i)
     for (int j = 0; j < kAnaSplits; ++j) SW_TRY(upload(p, work[i][j], &p->work[i][j]));
   return kOk;
@@ -420,7 +421,11 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
     rs += (9 - rs % 8) % 8;  // == 1 (mod 8) double2 slots: rings differ in bank group
     P.ring_stride = rs;
   }
-  std::vector<int2> work[2][kAnaSplits];
+  // analysis work lists: CTA items (r, first chunk c, checkpoint index of
+  // chunk c); items whose first chunk is full come first and the partial last
+  // chunks of the rows after them, longest first (stable, so rows stay
+  // together), so the short items fill the tail of the last wave
+  std::vector<int4> work[2][kAnaSplits];
   for (int which = 0; which < 2; ++which) {
     const int smax = R + which;
     for (int r = 0; r <= R; ++r) {
@@ -428,8 +433,14 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
       p->nchunks[which] += (nout + kChunk - 1) / kChunk;
       for (int ls = 0; ls < kAnaSplits; ++ls) {
         const int cpc = ana_chunks_per_cta(ls + 1);
-        for (int c = 0; c * kChunk < nout; c += cpc) work[which][ls].push_back(make_int2(r, c));
+        for (int c = 0; c * kChunk < nout; c += cpc)
+          work[which][ls].push_back(make_int4(r, c, ck_off[r] + c, 0));
       }
+    }
+    for (int ls = 0; ls < kAnaSplits; ++ls) {
+      auto len = [&](const int4& it) { return std::min(kChunk, smax - it.x + 1 - it.y * kChunk); };
+      std::stable_sort(work[which][ls].begin(), work[which][ls].end(),
+                       [&](const int4& u, const int4& v) { return len(u) > len(v); });
     }
   }
 

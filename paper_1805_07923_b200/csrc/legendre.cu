@@ -430,6 +430,16 @@ int launch_synthesis(const PlanDev& P, const SynArgs& a, int B, int mode, cudaSt
 namespace {
 
 constexpr int kAnaWarps = 4;
+
+// Zeros for s < r of row r (dense output): the CTA's warps take whole vectors,
+// lanes consecutive degrees (coalesced 16-byte stores, no index division).
+__device__ __forceinline__ void ana_zero_fill(const AnaArgs& a, double2* out, int r, int warp,
+                                              int nwarps, int lane) {
+  for (int v = warp; v < a.nv; v += nwarps) {
+    double2* o = out + (size_t)v * a.out_vstride + (size_t)r * a.out_rstride;
+    for (int s = lane; s < r; s += 32) o[s] = make_double2(0.0, 0.0);
+  }
+}
 constexpr int kQS = kChunk + 4;   // A-tile row stride (doubles), == 4 mod 16
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
@@ -487,16 +497,11 @@ ana_kernel(PlanDev P, AnaArgs a) {
 
   const double* x = a.x + (size_t)blockIdx.y * a.xl.mstride;
   double2* out = a.out + (size_t)blockIdx.y * a.out_mstride;
-  const int2 wk = a.work[blockIdx.x];
+  const int4 wk = a.work[blockIdx.x];
   const int r = wk.x, c = wk.y + warp / LSPLIT, half = warp % LSPLIT;
   const int nout = a.smax - r + 1;
 
-  if (a.zero_fill && wk.y == 0 && warp == 0) {
-    for (int idx = lane; idx < a.nv * r; idx += 32) {
-      const int v = idx / r, s = idx - v * r;
-      out[(size_t)v * a.out_vstride + (size_t)r * a.out_rstride + s] = make_double2(0.0, 0.0);
-    }
-  }
+  if (a.zero_fill && wk.y == 0) ana_zero_fill(a, out, r, warp, blockDim.x >> 5, lane);
   const bool active = c * kChunk < nout;
 
   double acc[2][2][NT][2];
@@ -510,7 +515,7 @@ ana_kernel(PlanDev P, AnaArgs a) {
   const int k0 = c * kChunk;
   if (active) {
     bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
-    const double2* seeds = P.ckpt + (size_t)(P.ck_off[r] + c) * P.Jh;
+    const double2* seeds = P.ckpt + (size_t)(wk.z + (c - wk.y)) * P.Jh;
     const int nc = a.xl.nc, jh4 = a.xl.jh4;
     const double* xr = x + (size_t)r * jh4 * 2 * nc * 4;
     const int nblk = (P.Jh + 31) >> 5;
@@ -729,15 +734,10 @@ ana_dfma_kernel(PlanDev P, AnaArgs a) {
   double* bring = bs + kChunk;                // [kBDepth][2][NT * 32]
   const double* x = a.x + (size_t)blockIdx.y * a.xl.mstride;
   double2* out = a.out + (size_t)blockIdx.y * a.out_mstride;
-  const int2 wk = a.work[blockIdx.x];
+  const int4 wk = a.work[blockIdx.x];
   const int r = wk.x, c = wk.y + warp / LSPLIT, half = warp % LSPLIT;
   const int nout = a.smax - r + 1;
-  if (a.zero_fill && wk.y == 0 && warp == 0) {
-    for (int idx = lane; idx < a.nv * r; idx += 32) {
-      const int v = idx / r, s = idx - v * r;
-      out[(size_t)v * a.out_vstride + (size_t)r * a.out_rstride + s] = make_double2(0.0, 0.0);
-    }
-  }
+  if (a.zero_fill && wk.y == 0) ana_zero_fill(a, out, r, warp, blockDim.x >> 5, lane);
   const bool active = c * kChunk < nout;
   const int k0 = c * kChunk;
   const int par = lane >> 4;   // degree parity of this lane: x parity S (0) or D (1)
@@ -746,7 +746,7 @@ ana_dfma_kernel(PlanDev P, AnaArgs a) {
   for (int v = 0; v < NV; ++v) { acc[v][0] = 0.0; acc[v][1] = 0.0; }
   if (active) {
     bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
-    const double2* seeds = P.ckpt + (size_t)(P.ck_off[r] + c) * P.Jh;
+    const double2* seeds = P.ckpt + (size_t)(wk.z + (c - wk.y)) * P.Jh;
     const int nc = a.xl.nc, jh4 = a.xl.jh4;
     const double* xr = x + (size_t)r * jh4 * 2 * nc * 4;
     const int nblk = (P.Jh + 31) >> 5;
@@ -995,17 +995,12 @@ ana_tma_kernel(PlanDev P, AnaArgs a) {
 
   const double* x = a.x + (size_t)blockIdx.y * a.xl.mstride;
   double2* out = a.out + (size_t)blockIdx.y * a.out_mstride;
-  const int2 wk = a.work[blockIdx.x];
+  const int4 wk = a.work[blockIdx.x];
   const int r = wk.x, c = wk.y + warp;
   const int nout = a.smax - r + 1;
   const bool active = c * kChunk < nout;
 
-  if (a.zero_fill && wk.y == 0 && warp == 0) {
-    for (int idx = lane; idx < a.nv * r; idx += 32) {
-      const int v = idx / r, s = idx - v * r;
-      out[(size_t)v * a.out_vstride + (size_t)r * a.out_rstride + s] = make_double2(0.0, 0.0);
-    }
-  }
+  if (a.zero_fill && wk.y == 0) ana_zero_fill(a, out, r, warp, blockDim.x >> 5, lane);
   const int jh4 = a.xl.jh4;
   const int nblk = (P.Jh + 31) >> 5;
   const double* xr = x + (size_t)r * jh4 * 2 * nc * 4;
@@ -1034,7 +1029,7 @@ ana_tma_kernel(PlanDev P, AnaArgs a) {
       for (int n = 0; n < NT; ++n) { acc[p][mt][n][0] = 0.0; acc[p][mt][n][1] = 0.0; }
 
   const int k0 = c * kChunk;
-  const double2* seeds = P.ckpt + (size_t)(P.ck_off[r] + (active ? c : 0)) * P.Jh;
+  const double2* seeds = P.ckpt + (size_t)(wk.z + (active ? c - wk.y : 0)) * P.Jh;
   if (active) bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
   const int ncol = 2 * a.nv;
   double2 sd_nx = make_double2(0.0, 0.0);

@@ -36,7 +36,8 @@ struct AnaArgs {
   long long out_rstride;
   int smax;                // highest degree written (R, or R+1 for the H shift)
   int zero_fill;           // also write zeros for s < r
-  const int2* work;        // (r, first chunk) list, one CTA (ana_warps_per_cta chunks) each
+  const int4* work;        // (r, first chunk c, checkpoint index ck_off[r] + c, 0) list,
+                           // one CTA (ana_warps_per_cta chunks) each
   long long out_mstride;   // complex elements between members (blockIdx.y)
   int nmembers;
   int short_tiles;         // run half-empty last chunks without their upper m-tile
