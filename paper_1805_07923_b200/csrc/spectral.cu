@@ -121,13 +121,16 @@ __global__ void eval_fi_kernel(int R, ModelConsts c, const double2* x, double2* 
        idx += (long long)gridDim.x * blockDim.x) {
     const long long m = idx / plane;
     const int rs = (int)(idx - m * plane);
-    const int s = rs % (R + 1);
-    if ((rs / (R + 1)) % rf.mod != rf.rank) continue;
+    const int r = rs / (R + 1), s = rs - r * (R + 1);
+    if (r % rf.mod != rf.rank) continue;
     const double lam = lam_of(s, c.radius);
     const double nl = c.nu * lam;
     const double2* xm = x + m * 3 * plane + rs;
     double2* om = out + m * 3 * plane + rs;
-    const double2 ph = xm[0], ze = xm[plane], de = xm[2 * plane];
+    const double2 z0 = make_double2(0.0, 0.0);
+    // s < r: structurally zero input (spharm.py:6-10), not read
+    const bool up = s >= r;
+    const double2 ph = up ? xm[0] : z0, ze = up ? xm[plane] : z0, de = up ? xm[2 * plane] : z0;
     om[0] = make_double2(-c.phi_bar * de.x + nl * ph.x, -c.phi_bar * de.y + nl * ph.y);
     om[plane] = make_double2(nl * ze.x, nl * ze.y);
     om[2 * plane] = make_double2(-lam * ph.x + nl * de.x, -lam * ph.y + nl * de.y);
@@ -185,7 +188,7 @@ __global__ void resize_kernel(const double2* in, int rin, double2* out, int rout
     const int r = rs / (rout + 1), s = rs - r * (rout + 1);
     if (r % rf.mod != rf.rank) continue;
     double2 v = make_double2(0.0, 0.0);
-    if (r <= rin && s <= rin) v = in[m * (long long)(rin + 1) * (rin + 1) + (long long)r * (rin + 1) + s];
+    if (r <= rin && s <= rin && s >= r) v = in[m * (long long)(rin + 1) * (rin + 1) + (long long)r * (rin + 1) + s];
     out[idx] = v;
   }
 }
@@ -267,6 +270,8 @@ __global__ void __launch_bounds__(256) spec_combine_multi_kernel(MultiCombineArg
   const int ro = a.rout;
   if (r > a.ext[o] || s > a.ext[o]) return;
   double2 acc = make_double2(0.0, 0.0);
+  // s < r is structurally zero in every spectral state (spharm.py:6-10): no reads
+  if (s >= r)
   for (int k = a.off[o]; k < a.off[o + 1]; ++k) {
     const int ri = a.rin[k];
     if (r <= ri && s <= ri) {
@@ -291,6 +296,7 @@ __global__ void spec_combine_kernel(SpecCombineArgs a, long long nmat, RowFilter
     const int r = rs / (ro + 1), s = rs - r * (ro + 1);
     if (r % rf.mod != rf.rank) continue;
     double2 acc = make_double2(0.0, 0.0);
+    if (s >= r)   // s < r: structurally zero, no reads
     for (int k = 0; k < a.n; ++k) {
       const int ri = a.rin[k];
       if (r <= ri && s <= ri) {
@@ -314,9 +320,16 @@ __global__ void sweep_node_kernel(int R, ModelConsts c, double beta, SpecCombine
        idx += (long long)gridDim.x * blockDim.x) {
     const long long m = idx / plane;
     const int rs = (int)(idx - m * plane);
-    const int s = rs % (R + 1);
-    if ((rs / (R + 1)) % rf.mod != rf.rank) continue;
+    const int r = rs / (R + 1), s = rs - r * (R + 1);
+    if (r % rf.mod != rf.rank) continue;
     const long long o = m * 3 * plane + rs;
+    if (s < r) {
+      // structurally zero coefficients (spharm.py:6-10): zeros out, no term reads
+      const double2 z = make_double2(0.0, 0.0);
+      theta[o] = z; theta[o + plane] = z; theta[o + 2 * plane] = z;
+      fi[o] = z; fi[o + plane] = z; fi[o + 2 * plane] = z;
+      continue;
+    }
     double2 b[3];
 #pragma unroll
     for (int f = 0; f < 3; ++f) b[f] = make_double2(0.0, 0.0);
