@@ -99,10 +99,12 @@ __device__ __forceinline__ double2 fetch_coef(const double2* f, int srcR, int r,
   return f[(size_t)r * (srcR + 1) + s];
 }
 
-__device__ __forceinline__ double inv_lap(int s, double radius) {
+// (1 / lambda_s) / a = -a / (s (s + 1)), lambda_s = -s (s + 1) / a^2 (swe.py:186-189,
+// spharm.py:321-333, s = 0 gauged to 0): one division instead of the two of
+// forming lambda_s and inverting it
+__device__ __forceinline__ double inv_lap_a(int s, double radius) {
   if (s <= 0) return 0.0;
-  const double lam = (-(double)s * (s + 1.0)) / (radius * radius);
-  return 1.0 / lam;
+  return -radius / ((double)s * (s + 1.0));
 }
 
 // Raw per-lane loads of one chunk (degree s = r + k0 + lane) kept in registers
@@ -188,9 +190,8 @@ __device__ __forceinline__ void stage_chunk(const ChunkRegs<B, MODE>& c, double2
     v[1] = make_double2(-r * c.raw[0].y + hc.x, r * c.raw[0].x + hc.y);
   } else {
     // psi = invlap(zeta), chi = invlap(delta) (swe.py:186-187), then 1/a (swe.py:189)
-    const double ia = 1.0 / radius;
-    const double s0 = inv_lap(s, radius) * ia, sp = inv_lap(s + 1, radius) * ia,
-                 sm = inv_lap(s - 1, radius) * ia;
+    const double s0 = inv_lap_a(s, radius), sp = inv_lap_a(s + 1, radius),
+                 sm = inv_lap_a(s - 1, radius);
     const double2 hpsi = hfold(c.raw[2], c.raw[3], c.eps0, c.eps1, s, sp, sm);
     const double2 hchi = hfold(c.raw[4], c.raw[5], c.eps0, c.eps1, s, sp, sm);
     v[0] = make_double2(-r * c.raw[1].y * s0 - hpsi.x, r * c.raw[1].x * s0 - hpsi.y);  // U/a
@@ -249,10 +250,11 @@ syn_kernel(PlanDev P, SynArgs a) {
   }
   // warps -> (row, chunk range); a warp never straddles the rows
   int wrow = 0, cb = 0, ce = 0;
+  int w1 = NSPLIT;   // warps [0, w1) take row 0, [w1, NSPLIT) row 1
   if (NSPLIT == 1) {
     wrow = -1;  // the single warp walks both rows
   } else {
-    int w1 = two ? (NSPLIT * nch[0] + (nch[0] + nch[1]) / 2) / (nch[0] + nch[1]) : NSPLIT;
+    w1 = two ? (NSPLIT * nch[0] + (nch[0] + nch[1]) / 2) / (nch[0] + nch[1]) : NSPLIT;
     w1 = max(1, min(w1, two ? NSPLIT - 1 : NSPLIT));
     if (warp < w1) {
       wrow = 0;
@@ -350,11 +352,8 @@ syn_kernel(PlanDev P, SynArgs a) {
       const int j = lg * kSynLat + lj;
       if (j >= P.Jh) continue;
       double2 e = make_double2(0.0, 0.0), o = e;
-      for (int w = 0; w < NSPLIT; ++w) {
-        // warp w's row
-        int w1 = two ? (NSPLIT * nch[0] + (nch[0] + nch[1]) / 2) / (nch[0] + nch[1]) : NSPLIT;
-        w1 = max(1, min(w1, two ? NSPLIT - 1 : NSPLIT));
-        if ((w < w1 ? 0 : 1) != ir) continue;
+      const int wb = ir == 0 ? 0 : w1, we = ir == 0 ? w1 : NSPLIT;   // the row's warps
+      for (int w = wb; w < we; ++w) {
         const double2* src = red + ((size_t)w * B * kSynLat + (size_t)b * kSynLat + lj) * 2;
         e.x += src[0].x; e.y += src[0].y;
         o.x += src[1].x; o.y += src[1].y;
