@@ -174,7 +174,9 @@ __device__ __forceinline__ void put_x(double* x, const XLayout& L, int v, int r,
 // ---------------------------------------------------------------------------
 // RINGS: write each pair's ring (north, south) contiguously, rings_out[f][jh][il]
 // (double2, grid_fstride in double2), the layout swe_prod_kernel reads coalesced.
-template <bool BIGP, bool RINGS = false>
+// K15 > 0: n_lon = 15 * 32 K15, one pair per CTA, 256 threads: the ring is
+// filled in natural order and transformed by swfft::ring_fft15 (reg_fft.cuh).
+template <bool BIGP, bool RINGS = false, int K15 = 0>
 __global__ void __launch_bounds__(256, 2) f2g_kernel(PlanDev P, const double2* eo, long long eo_fstride, double* grid,
                            long long grid_fstride, int lnp, int jh_begin, int jh_end) {
   pdl_wait();
@@ -185,9 +187,10 @@ __global__ void __launch_bounds__(256, 2) f2g_kernel(PlanDev P, const double2* e
   const int jh0 = jh_begin + blockIdx.x * np;
   PlanDev Q = P;
   Q.Jh = jh_end;  // pairs >= jh_end are not this launch's (fill_rings bounds on Q.Jh)
-  fill_rings(rings, Q, eo + (size_t)f * eo_fstride, 0, 1, np, lnp, jh0);
+  fill_rings(rings, Q, eo + (size_t)f * eo_fstride, 0, 1, np, lnp, jh0, K15 > 0);
   __syncthreads();
-  fft_inverse<BIGP>(rings, np, P);
+  if constexpr (K15 > 0) swfft::ring_fft15<K15, true>(rings, P.tw);
+  else fft_inverse<BIGP>(rings, np, P);
   if (RINGS) {
     double2* out = reinterpret_cast<double2*>(grid) + (size_t)f * grid_fstride;
     for (int i = 0; i < np && jh0 + i < jh_end; ++i) {
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(256, 2) f2g_kernel(PlanDev P, const double2* e
 // vector, weight w).  MODE 1: div/curl (fields U, V -> 4 vectors
 // [P-div, H-div, P-curl, H-curl], weight w / (1 - mu^2)).
 // ---------------------------------------------------------------------------
-template <int MODE, bool BIGP>
+template <int MODE, bool BIGP, int K15 = 0>
 __global__ void __launch_bounds__(256, 2) g2f_kernel(PlanDev P, const double* grid, const double* grid2,
                            long long grid_fstride, double* x, XLayout xl, int lnp) {
   pdl_wait();
@@ -253,13 +256,18 @@ __global__ void __launch_bounds__(256, 2) g2f_kernel(PlanDev P, const double* gr
           const int q = (NIN == 1) ? 0 : idx / (P.I << lnp);
           const int rem = idx - q * (P.I << lnp);
           const int il = rem >> lnp, i = rem & (np - 1);
-          rings[(size_t)(q * np + i) * P.ring_stride + P.rev[il]] = z[u];
+          rings[(size_t)(q * np + i) * P.ring_stride + (K15 > 0 ? swfft::pad_idx(il) : P.rev[il])] = z[u];
         }
       }
     }
   }
   __syncthreads();
-  fft_forward<BIGP>(rings, NIN * np, P);
+  if constexpr (K15 > 0) {
+#pragma unroll 1
+    for (int q = 0; q < NIN; ++q) swfft::ring_fft15<K15, false>(rings + (size_t)q * P.ring_stride, P.tw);
+  } else {
+    fft_forward<BIGP>(rings, NIN * np, P);
+  }
   // mode 0: field f is vector f of one member; mode 1: pair f is member f (4 vectors)
   double* xf = x + (MODE == 0 ? 0 : (size_t)f * xl.mstride);
   for (int idx = threadIdx.x; idx < ((P.R + 1) << lnp); idx += blockDim.x) {
@@ -833,7 +841,7 @@ __global__ void __launch_bounds__(256, 2) swe_grid_kernel(PlanDev P, const doubl
 // transformed pairwise through 2 rings, each pair completing its analysis
 // vectors: (A1, ZU) -> v1, v6; (A2, ZV) -> v2, v5; (PU, PV) -> v0, v4; KE -> v3.
 // ---------------------------------------------------------------------------
-template <bool NONLIN, bool BIGP, bool RINGS = false>
+template <bool NONLIN, bool BIGP, bool RINGS = false, int K15 = 0>
 __global__ void __launch_bounds__(256, 1) swe_prod_kernel(PlanDev P, const double* grids,
                                                           long long gfield, long long gmember,
                                                           double* x, XLayout xl, double omega,
@@ -883,12 +891,17 @@ __global__ void __launch_bounds__(256, 1) swe_prod_kernel(PlanDev P, const doubl
       } else {                  // KE = (U^2 + V^2) / (2 (1 - mu^2))
         a = d2(0.5 * (U.x * U.x + V.x * V.x) * ic2, 0.5 * (U.y * U.y + V.y * V.y) * ic2);
       }
-      const int p = P.rev[il];
+      const int p = K15 > 0 ? swfft::pad_idx(il) : P.rev[il];
       rings[p] = a;
       if (nr == 2) rings[RS + p] = b;
     }
     __syncthreads();
-    fft_forward<BIGP>(rings, nr, P);
+    if constexpr (K15 > 0) {
+      swfft::ring_fft15<K15, false>(rings, P.tw);
+      if (nr == 2) swfft::ring_fft15<K15, false>(rings + RS, P.tw);
+    } else {
+      fft_forward<BIGP>(rings, nr, P);
+    }
     for (int r = threadIdx.x; r <= P.R; r += blockDim.x) {
       double2 An, As, Bn = d2(0.0, 0.0), Bs = Bn;
       get_pair(rings, P, r, An, As);
@@ -996,16 +1009,55 @@ int g2f_reg_launch(const PlanDev& P, const double* grid, const double* grid2,
     case 24: { constexpr int KK = 24; return CALL; }                              \
   }
 
+// n_lon = 15 * 32 K with one pair per CTA: the ring_fft15 kernels (SWSDC_FFT15=0 disables)
+int fft15_path(const PlanDev& P, int lnp) {
+  static const int knob = env_int("SWSDC_FFT15", 1);
+  return (knob != 0 && lnp == 0) ? swfft::fft15_k(P.I) : 0;
+}
+
+#define SWSDC_K15_SWITCH(K_, CALL)                                                \
+  switch (K_) {                                                                   \
+    case 1: { constexpr int KK = 1; return CALL; }                                \
+    case 2: { constexpr int KK = 2; return CALL; }                                \
+    case 4: { constexpr int KK = 4; return CALL; }                                \
+    case 8: { constexpr int KK = 8; return CALL; }                                \
+    case 16: { constexpr int KK = 16; return CALL; }                              \
+  }
+
+template <bool BIGP, bool RINGS, int K15>
+int f2g_launch_k(const PlanDev& P, const double2* eo, long long eo_fstride, double* grid,
+                 long long grid_fstride, int nf, int jh_begin, int jh_end, int lnp, int threads,
+                 cudaStream_t st) {
+  const int np = 1 << lnp;
+  const size_t smem = sizeof(double2) * np * P.ring_stride;
+  SW_TRY(set_smem((const void*)f2g_kernel<BIGP, RINGS, K15>, smem));
+  dim3 gridDim((jh_end - jh_begin + np - 1) / np, nf);
+  if (gridDim.x == 0) return kOk;
+  StageScope sc("fourier_to_grid", st);
+  SW_CUDA(launch_pdl(f2g_kernel<BIGP, RINGS, K15>, dim3(gridDim), dim3(threads), smem, st, P, eo, eo_fstride, grid, grid_fstride, lnp, jh_begin, jh_end));
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
 template <bool BIGP, bool RINGS = false>
 int f2g_launch(const PlanDev& P, const double2* eo, long long eo_fstride, double* grid,
                long long grid_fstride, int nf, int jh_begin, int jh_end, cudaStream_t st) {
   const int lnp = pairs_log2(P, 1), np = 1 << lnp;
-  const size_t smem = sizeof(double2) * np * P.ring_stride;
-  SW_TRY(set_smem((const void*)f2g_kernel<BIGP, RINGS>, smem));
-  dim3 gridDim((jh_end - jh_begin + np - 1) / np, nf);
-  if (gridDim.x == 0) return kOk;
-  StageScope sc("fourier_to_grid", st);
-  SW_CUDA(launch_pdl(f2g_kernel<BIGP, RINGS>, dim3(gridDim), dim3(pick_threads(np * max_butterflies(P), BIGP)), smem, st, P, eo, eo_fstride, grid, grid_fstride, lnp, jh_begin, jh_end));
+  SWSDC_K15_SWITCH(fft15_path(P, lnp), (f2g_launch_k<false, RINGS, KK>(P, eo, eo_fstride, grid, grid_fstride, nf, jh_begin, jh_end, lnp, 256, st)));
+  return f2g_launch_k<BIGP, RINGS, 0>(P, eo, eo_fstride, grid, grid_fstride, nf, jh_begin, jh_end,
+                                      lnp, pick_threads(np * max_butterflies(P), BIGP), st);
+}
+
+template <int MODE, bool BIGP, int K15>
+int g2f_launch_k(const PlanDev& P, const double* grid, const double* grid2, long long grid_fstride,
+                 double* x, const XLayout& xl, int nf, int lnp, int threads, cudaStream_t st) {
+  const int nin = MODE == 0 ? 1 : 2;
+  const int np = 1 << lnp;
+  const size_t smem = sizeof(double2) * nin * np * P.ring_stride;
+  dim3 gridDim((P.Jh + np - 1) / np, nf);
+  SW_TRY(set_smem((const void*)g2f_kernel<MODE, BIGP, K15>, smem));
+  StageScope sc(MODE == 0 ? "grid_to_fourier" : "grid_to_fourier_divcurl", st);
+  SW_CUDA(launch_pdl(g2f_kernel<MODE, BIGP, K15>, dim3(gridDim), dim3(threads), smem, st, P, grid, grid2, grid_fstride, x, xl, lnp));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -1015,13 +1067,9 @@ int g2f_launch(const PlanDev& P, const double* grid, const double* grid2, long l
                double* x, const XLayout& xl, int nf, cudaStream_t st) {
   const int nin = MODE == 0 ? 1 : 2;
   const int lnp = pairs_log2(P, nin), np = 1 << lnp;
-  const size_t smem = sizeof(double2) * nin * np * P.ring_stride;
-  dim3 gridDim((P.Jh + np - 1) / np, nf);
-  SW_TRY(set_smem((const void*)g2f_kernel<MODE, BIGP>, smem));
-  StageScope sc(MODE == 0 ? "grid_to_fourier" : "grid_to_fourier_divcurl", st);
-  SW_CUDA(launch_pdl(g2f_kernel<MODE, BIGP>, dim3(gridDim), dim3(pick_threads(nin * np * max_butterflies(P), BIGP)), smem, st, P, grid, grid2, grid_fstride, x, xl, lnp));
-  SW_LAUNCH_CHECK();
-  return kOk;
+  SWSDC_K15_SWITCH(fft15_path(P, lnp), (g2f_launch_k<MODE, false, KK>(P, grid, grid2, grid_fstride, x, xl, nf, lnp, 256, st)));
+  return g2f_launch_k<MODE, BIGP, 0>(P, grid, grid2, grid_fstride, x, xl, nf, lnp,
+                                     pick_threads(nin * np * max_butterflies(P), BIGP), st);
 }
 
 template <bool NONLIN, bool BIGP>
@@ -1086,19 +1134,28 @@ int swe_fwd_reg_launch(const PlanDev& P, const double2* grids, long long gfield,
   return kOk;
 }
 
+template <bool NONLIN, bool BIGP, int K15>
+int swe_prod_launch_k(const PlanDev& P, const double* grids, long long gfield, long long gmember,
+                      double* x, const XLayout& xl, int nmembers, double omega, double radius,
+                      int jh_begin, int jh_end, cudaStream_t st) {
+  // grids in the ring layout (f2g_kernel<., true>): gfield / gmember in double2
+  const size_t smem = sizeof(double2) * 2 * P.ring_stride;
+  SW_TRY(set_smem((const void*)swe_prod_kernel<NONLIN, BIGP, true, K15>, smem));
+  dim3 gridDim(jh_end - jh_begin, nmembers);
+  if (gridDim.x == 0) return kOk;
+  StageScope sc("swe_products", st);
+  SW_CUDA(launch_pdl(swe_prod_kernel<NONLIN, BIGP, true, K15>, dim3(gridDim), dim3(BIGP && K15 == 0 ? 128 : 256), smem, st, P, grids, gfield, gmember, x, xl, omega, radius, jh_begin));
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
 template <bool NONLIN, bool BIGP>
 int swe_prod_launch(const PlanDev& P, const double* grids, long long gfield, long long gmember,
                     double* x, const XLayout& xl, int nmembers, double omega, double radius,
                     int jh_begin, int jh_end, cudaStream_t st) {
-  // grids in the ring layout (f2g_kernel<., true>): gfield / gmember in double2
-  const size_t smem = sizeof(double2) * 2 * P.ring_stride;
-  SW_TRY(set_smem((const void*)swe_prod_kernel<NONLIN, BIGP, true>, smem));
-  dim3 gridDim(jh_end - jh_begin, nmembers);
-  if (gridDim.x == 0) return kOk;
-  StageScope sc("swe_products", st);
-  SW_CUDA(launch_pdl(swe_prod_kernel<NONLIN, BIGP, true>, dim3(gridDim), dim3(BIGP ? 128 : 256), smem, st, P, grids, gfield, gmember, x, xl, omega, radius, jh_begin));
-  SW_LAUNCH_CHECK();
-  return kOk;
+  SWSDC_K15_SWITCH(fft15_path(P, 0), (swe_prod_launch_k<NONLIN, false, KK>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, jh_begin, jh_end, st)));
+  return swe_prod_launch_k<NONLIN, BIGP, 0>(P, grids, gfield, gmember, x, xl, nmembers, omega,
+                                            radius, jh_begin, jh_end, st);
 }
 
 }  // namespace

@@ -116,27 +116,30 @@ __host__ __device__ constexpr bool reg_fft_k_ok(int K) {
 
 // Per-lane twiddles of the cross-lane stages h = 16, 8, 4: W_{2h}^(l mod h)
 // on the upper lane of each pair, 1 on the lower one.
+// tws: stride of tw relative to an N-point table (a sub-transform of a longer
+// ring reads the longer ring's table: W_N^e = tw[e * tws]).
 template <int K, bool INV>
-__device__ __forceinline__ void cross_twiddles(double2 (&wst)[3], const double2* tw, int lane) {
+__device__ __forceinline__ void cross_twiddles(double2 (&wst)[3], const double2* tw, int lane,
+                                               int tws = 1) {
 #pragma unroll
   for (int st = 0; st < 3; ++st) {
     const int h = 16 >> st;
     const int j = lane & (h - 1);
-    wst[st] = (lane & h) ? tw_at(tw, j * (16 / h) * K, INV) : mk2(1.0, 0.0);
+    wst[st] = (lane & h) ? tw_at(tw, j * (16 / h) * K * tws, INV) : mk2(1.0, 0.0);
   }
 }
 
 // Full N-point transform (see the header comment); wst from cross_twiddles.
 template <int K, bool INV>
 __device__ __forceinline__ void ring_fft(double2 (&v)[K], const double2* tw, int lane,
-                                         const double2 (&wst)[3]) {
+                                         const double2 (&wst)[3], int tws = 1) {
   dft_k<K, INV>(v, tw);
   // W_N^(lane m1) from the gathered powers W_N^(lane 2^b) (2^b < K, so
   // lane 2^b < N) by at most 4 products: 5 table gathers instead of K - 1
   constexpr int NB = K > 16 ? 5 : K > 8 ? 4 : K > 4 ? 3 : K > 2 ? 2 : 1;
   double2 wp[NB];
 #pragma unroll
-  for (int b = 0; b < NB; ++b) wp[b] = tw_at(tw, lane << b, INV);
+  for (int b = 0; b < NB; ++b) wp[b] = tw_at(tw, (lane << b) * tws, INV);
 #pragma unroll
   for (int m1 = 1; m1 < K; ++m1) {
     double2 w = mk2(1.0, 0.0);
@@ -171,6 +174,84 @@ __device__ __forceinline__ void ring_fft(double2 (&v)[K], const double2* tw, int
       v[q] = d;
     }
   }
+}
+
+// 15-point DFT in registers, natural order in and out: prime-factor
+// (Good-Thomas) 3 x 5 with no twiddles -- input n = (5 na + 3 nb) mod 15,
+// output k = (10 ka + 6 kb) mod 15.
+template <bool INV>
+__device__ __forceinline__ void dft15(double2 (&v)[15]) {
+  double2 t[3][5];
+#pragma unroll
+  for (int na = 0; na < 3; ++na) {
+#pragma unroll
+    for (int nb = 0; nb < 5; ++nb) t[na][nb] = v[(5 * na + 3 * nb) % 15];
+    small_dft<5>(t[na], INV);
+  }
+#pragma unroll
+  for (int kb = 0; kb < 5; ++kb) {
+    double2 u[3] = {t[0][kb], t[1][kb], t[2][kb]};
+    small_dft<3>(u, INV);
+#pragma unroll
+    for (int ka = 0; ka < 3; ++ka) v[(10 * ka + 6 * kb) % 15] = u[ka];
+  }
+}
+
+// In-place FFT of one ring of N = 15 * 32 K points in shared memory (padded
+// slots pad_idx, natural order in and out), by a CTA of >= 256 threads:
+// N = N1 x 15 with N1 = 32 K, n = n1 + N1 n2, k = k2 + 15 k1.
+//   A. thread n1: 15-point DFT over n2 in registers, twiddle W_N^(n1 k2),
+//      written back to the same slots (no barrier between read and write);
+//   B. warp: column k2 (contiguous N1 points) through the register FFT
+//      ring_fft<K> on the N-point table at stride 15, results scattered to
+//      k2 + 15 k1 once every column has been read.
+// Three CTA barriers instead of one per radix stage, and no digit reversal.
+template <int K, bool INV>
+__device__ void ring_fft15(double2* ring, const double2* tw) {
+  constexpr int N1 = 32 * K;
+  const int nthr = blockDim.x;
+  for (int n1 = threadIdx.x; n1 < N1; n1 += nthr) {
+    double2 v[15];
+#pragma unroll
+    for (int n2 = 0; n2 < 15; ++n2) v[n2] = ring[pad_idx(n1 + N1 * n2)];
+    dft15<INV>(v);
+#pragma unroll
+    for (int k2 = 1; k2 < 15; ++k2)
+      if (n1 != 0) v[k2] = cmul(v[k2], tw_at(tw, n1 * k2, INV));
+#pragma unroll
+    for (int k2 = 0; k2 < 15; ++k2) ring[pad_idx(n1 + N1 * k2)] = v[k2];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = nthr >> 5;
+  double2 c[2][K];   // nw >= 8: at most two of the 15 columns per warp
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int k2 = warp + i * nw;
+    if (k2 < 15) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) c[i][k] = ring[pad_idx(N1 * k2 + 32 * k + lane)];
+    }
+  }
+  __syncthreads();
+  double2 wst[3];
+  cross_twiddles<K, INV>(wst, tw, lane, 15);
+  const int b = (int)(__brev((unsigned)lane) >> 27);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int k2 = warp + i * nw;
+    if (k2 < 15) {
+      ring_fft<K, INV>(c[i], tw, lane, wst, 15);
+#pragma unroll
+      for (int m1 = 0; m1 < K; ++m1) ring[pad_idx(k2 + 15 * (m1 + K * b))] = c[i][m1];
+    }
+  }
+  __syncthreads();
+}
+
+// Ring length with a ring_fft15 path: N = 15 * 32 K, K a power of two <= 16.
+__host__ __device__ constexpr int fft15_k(int n) {
+  return (n % 480 == 0 && (n / 480 == 1 || n / 480 == 2 || n / 480 == 4 || n / 480 == 8 ||
+                           n / 480 == 16)) ? n / 480 : 0;
 }
 
 // Output index held by (lane, slot m1) after ring_fft.

@@ -139,3 +139,35 @@ def test_tma_and_forced_split_variants_match_reference(tmp_path):
                              text=True, env={**os.environ, **env}, timeout=300)
         assert out.returncode == 0, out.stderr[-2000:]
         assert float(out.stdout.strip().splitlines()[-1]) < TOL, (env, out.stdout)
+
+
+@pytest.mark.parametrize("R,I,J", [(63, 1920, 96), (31, 3840, 48), (47, 1920, 73)])
+def test_long_rings_match_oracle(R, I, J):
+    """n_lon = 15 * 32 K rings (T639 / T1279 grids: one latitude pair per CTA)
+    take the ring_fft15 kernels (15-point prime-factor DFT + register FFTs of
+    32 K points) in synthesize / analyze / div-curl and in the split F_E path;
+    small truncations keep the numpy oracle cheap."""
+    import swsdc_oracle as orc
+    from paper_1805_07923_b200 import spharm, swe, workloads
+    plan = plan_for(R, I, J)
+    oplan = orc.OraclePlan(R, I, J)
+    c = workloads.transform_batch(R, 3)
+    g = plan.synthesize(torch.as_tensor(c).cuda()).cpu().numpy()
+    want = np.stack([oplan.synthesize(ci) for ci in c])
+    assert rel_err(g, want) < TOL
+    back = plan.analyze(torch.as_tensor(want).cuda()).cpu().numpy()
+    assert rel_err(back, np.stack([oplan.analyze(gi) for gi in want])) < TOL
+    u, v = plan.synthesize_pair_cos_gradient(c[0], c[1])
+    ou, ov = oplan.synth_uv(c[0], c[1])
+    assert rel_err(u, ou) < TOL and rel_err(v, ov) < TOL
+    d, k = plan.analyze_vector_div_curl(want[0], want[1])
+    od, ok = oplan.anal_divcurl(want[0], want[1])
+    assert rel_err(d, od) < TOL and rel_err(k, ok) < TOL
+    params = swe.ModelParams(**workloads.EARTH)
+    orhs = orc.OracleRHS(oplan, orc.OracleParams(**workloads.EARTH))
+    x = workloads.seeded_state(R, 3)
+    fe = swe.ShallowWaterRHS(plan, params).eval_f_e(
+        swe.PrognosticState(torch.as_tensor(x).cuda())).numpy()
+    ofe = orhs.eval_fe(x)
+    for f in range(3):
+        assert rel_err(fe[f], ofe[f]) < TOL
