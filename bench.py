@@ -273,7 +273,6 @@ def run_ours(args, world, rank, local):
             dist.barrier()
         torch.cuda.synchronize()
         l0 = _lib.launch_count()
-        _lib.profile_enable(True)
         for k in range(args.steps):
             flush_l2()
             starts[k].record()
@@ -283,8 +282,18 @@ def run_ours(args, world, rank, local):
         if dist:
             dist.barrier()
         launches = _lib.launch_count() - l0
-        stages = _lib.profile_collect()
-        _lib.profile_enable(False)
+    # Per-kernel durations for the roofline: the same K steps again with the
+    # library's per-launch CUDA events on the launching stream.  A separate pass,
+    # because an event pair around every launch serialises the kernels that
+    # programmatic dependent launch otherwise overlaps (~25% on this step): the
+    # timed region above carries no instrumentation.
+    _lib.profile_enable(True)
+    for k in range(args.steps):
+        flush_l2()
+        step()
+    torch.cuda.synchronize()
+    stages = _lib.profile_collect()
+    _lib.profile_enable(False)
     t_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     t_ms = max_over_ranks(t_ms, dist, dev)
     value = world * NF * args.steps / (t_ms * 1e-3)
