@@ -25,6 +25,7 @@
 // Analysis: the q tile (32 degrees x 128 latitudes) is generated into shared
 // memory and contracted over latitude with FP64 tensor-core DMMA
 // (mma.sync.m8n8k4.f64), so the latitude reduction happens inside the MMA.
+#include <algorithm>
 #include <type_traits>
 
 #include "common.cuh"
@@ -481,12 +482,14 @@ __host__ __device__ constexpr int ana_warp_doubles() {
   return kChunk * kQS + kChunk + kBDepth * 2 * NT * 32;
 }
 
-template <int NT, int LSPLIT>
-__global__ void __launch_bounds__(kAnaWarps * 32)
-ana_kernel(PlanDev P, AnaArgs a) {
-  pdl_wait();
-  pdl_trigger();
-  extern __shared__ __align__(16) double smem[];
+// One work item (r, first chunk, checkpoint index) of member m.  PERSIST: the
+// CTA continues with another item afterwards, so the warps of a chunk meet
+// once more after the split reduction (the half-0 warp reads the other warps'
+// shared memory, which their next item overwrites).  A persistent grid walking
+// the item list was measured (profiles/r01/experiments.md) and not kept.
+template <int NT, int LSPLIT, bool PERSIST>
+__device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, const int4 wk, int m,
+                                         double* smem) {
   constexpr int kWD = ana_warp_doubles<NT>();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -494,9 +497,8 @@ ana_kernel(PlanDev P, AnaArgs a) {
   double* bs = qs + kChunk * kQS;                                // [32] betas
   double* bring = bs + kChunk;                                   // [kBDepth][2][NT * 32]
 
-  const double* x = a.x + (size_t)blockIdx.y * a.xl.mstride;
-  double2* out = a.out + (size_t)blockIdx.y * a.out_mstride;
-  const int4 wk = a.work[blockIdx.x];
+  const double* x = a.x + (size_t)m * a.xl.mstride;
+  double2* out = a.out + (size_t)m * a.out_mstride;
   const int r = wk.x, c = wk.y + warp / LSPLIT, half = warp % LSPLIT;
   const int nout = a.smax - r + 1;
 
@@ -512,6 +514,16 @@ ana_kernel(PlanDev P, AnaArgs a) {
       for (int n = 0; n < NT; ++n) { acc[p][mt][n][0] = 0.0; acc[p][mt][n][1] = 0.0; }
 
   const int k0 = c * kChunk;
+  // epilogue scales g of this lane's output rows k0 + p + 2 (8 mt + g), fetched
+  // now so the load latency hides behind the contraction
+  double gsv[2][2];
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int k = k0 + p + 2 * (8 * mt + g);
+      gsv[p][mt] = (active && k < nout) ? P.gsc[(size_t)r * P.ldk + k] : 0.0;
+    }
   if (active) {
     bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
     const double2* seeds = P.ckpt + (size_t)(wk.z + (c - wk.y)) * P.Jh;
@@ -667,7 +679,11 @@ ana_kernel(PlanDev P, AnaArgs a) {
           }
     }
     asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
-    if (half > 0 || !active) return;
+    if (!active) return;
+    if (half > 0) {
+      if (PERSIST) asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
+      return;
+    }
     for (int h = 1; h < LSPLIT; ++h) {
       const double* src = smem + (size_t)(warp + h) * ana_warp_doubles<NT>();
 #pragma unroll
@@ -681,19 +697,19 @@ ana_kernel(PlanDev P, AnaArgs a) {
             acc[p][mt][n][1] += src[(e + 1) * 32 + lane];
           }
     }
+    if (PERSIST) asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
   } else if (!active) {
     return;
   }
 
   // epilogue: row k = k0 + p + 2 (8 mt + g); columns (re, im) of vector n*4 + t
-  const double* gr = P.gsc + (size_t)r * P.ldk;
 #pragma unroll
   for (int p = 0; p < 2; ++p)
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
       const int k = k0 + p + 2 * (8 * mt + g);
       if (k >= nout) continue;
-      const double gs = gr[k];
+      const double gs = gsv[p][mt];
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
         const int v = n * 4 + t;
@@ -702,6 +718,16 @@ ana_kernel(PlanDev P, AnaArgs a) {
               make_double2(acc[p][mt][n][0] * gs, acc[p][mt][n][1] * gs);
       }
     }
+}
+
+// One CTA per work item (grid: items x members).
+template <int NT, int LSPLIT>
+__global__ void __launch_bounds__(kAnaWarps * 32)
+ana_kernel(PlanDev P, AnaArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(16) double smem[];
+  ana_item<NT, LSPLIT, false>(P, a, a.work[blockIdx.x], blockIdx.y, smem);
 }
 
 // ---------------------------------------------------------------------------
