@@ -383,6 +383,8 @@ int launch_syn_t(const PlanDev& P, const SynArgs& a, cudaStream_t st) {
 
 // Warps per CTA so the grid offers ~2 resident warps per SM sub-partition.
 int pick_split(const PlanDev& P, int npairs, int nmembers) {
+  static const int knob = env_int("SWSDC_SYN_SPLIT", 0);   // tuning knob: force 1, 2 or 4
+  if (knob == 1 || knob == 2 || knob == 4) return knob;
   const long long base = (long long)npairs * ((P.Jh + kSynLat - 1) / kSynLat) * nmembers;
   if (base >= 1000) return 1;
   if (base >= 500) return 2;
