@@ -311,7 +311,11 @@ int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, dou
   const int nch = sh ? sh->nchunks[which] : p->nchunks[which];
   // TMA variant (<= 8 vectors) runs unsplit; otherwise split latitudes to fill waves
   const int nv0 = xl.nv < 16 ? xl.nv : 16;
-  const int lsplit = ana_uses_tma(nv0) ? 1 : pick_ana_split(nch, nmembers, nv0, P.Jh);
+  // ensembles: two members per CTA when each has <= 8 vectors (same q tiles, NT = 4)
+  const bool pairs = xl.nv <= 8 && ana_pairs_ok(xl.nv, nmembers);
+  const int lsplit = ana_uses_tma(nv0) ? 1
+                     : pairs ? pick_ana_split(nch, nmembers / 2, 16, P.Jh)
+                             : pick_ana_split(nch, nmembers, nv0, P.Jh);
   const int ls = lsplit - 1;
   for (int v0 = 0; v0 < xl.nv; v0 += 16) {
     AnaArgs a{};
@@ -330,7 +334,12 @@ int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, dou
     a.short_tiles = short_tiles;
     const int nw = sh ? sh->nwork[which][ls] : p->nwork[which][ls];
     if (nw == 0) continue;
-    SW_TRY(launch_analysis(P, a, nw, lsplit, st));
+    if (pairs) {
+      a.nmembers = nmembers / 2;
+      SW_TRY(launch_analysis_pairs(P, a, nw, lsplit, st));
+    } else {
+      SW_TRY(launch_analysis(P, a, nw, lsplit, st));
+    }
   }
   return kOk;
 }

@@ -489,9 +489,14 @@ __host__ __device__ constexpr int ana_warp_doubles() {
 // once more after the split reduction (the half-0 warp reads the other warps'
 // shared memory, which their next item overwrites).  A persistent grid walking
 // the item list was measured (profiles/r01/experiments.md) and not kept.
-template <int NT, int LSPLIT, bool PERSIST>
+// MP = 2: members 2m and 2m + 1 of an ensemble share the CTA -- n-tiles
+// [0, NT/2) come from the first member's x, [NT/2, NT) from the second's
+// (each member's layout holds NT/2 n-tiles, a.nv <= 4 NT/2 vectors) -- so the
+// q tile and the A fragments serve twice the columns.
+template <int NT, int LSPLIT, bool PERSIST, int MP = 1>
 __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, const int4 wk, int m,
                                          double* smem) {
+  static_assert(MP == 1 || (MP == 2 && NT % 4 == 0), "member pairs need NT / 2 even");
   constexpr int kWD = ana_warp_doubles<NT>();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -499,12 +504,16 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
   double* bs = qs + kChunk * kQS;                                // [32] betas
   double* bring = bs + kChunk;                                   // [kBDepth][2][NT * 32]
 
-  const double* x = a.x + (size_t)m * a.xl.mstride;
-  double2* out = a.out + (size_t)m * a.out_mstride;
+  const double* x = a.x + (size_t)(MP * m) * a.xl.mstride;
+  double2* out = a.out + (size_t)(MP * m) * a.out_mstride;
   const int r = wk.x, c = wk.y + warp / LSPLIT, half = warp % LSPLIT;
   const int nout = a.smax - r + 1;
 
-  if (a.zero_fill && wk.y == 0) ana_zero_fill(a, out, r, warp, blockDim.x >> 5, lane);
+  if (a.zero_fill && wk.y == 0) {
+#pragma unroll
+    for (int h = 0; h < MP; ++h)
+      ana_zero_fill(a, out + (size_t)h * a.out_mstride, r, warp, blockDim.x >> 5, lane);
+  }
   const bool active = c * kChunk < nout;
 
   double acc[2][2][NT][2];
@@ -563,10 +572,13 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
           const double* s0 = ip + 2 * lane;
           const double* s1 = s0 + poff;
           double* d0 = dst + 2 * lane;
+          // MP = 2: copies u >= NT / 4 read the second member (its tile u - NT / 4)
+          constexpr int UM = NT / (2 * MP);
 #pragma unroll
           for (int u = 0; u < NT / 2; ++u) {
-            cp_async16_ana(d0 + 64 * u, s0 + 64 * u);
-            cp_async16_ana(d0 + NT * 32 + 64 * u, s1 + 64 * u);
+            const size_t so = (size_t)(u % UM) * 64 + (MP == 2 && u >= UM ? (size_t)a.xl.mstride : 0);
+            cp_async16_ana(d0 + 64 * u, s0 + so);
+            cp_async16_ana(d0 + NT * 32 + 64 * u, s1 + so);
           }
         } else {
 #pragma unroll
@@ -714,22 +726,24 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
       const double gs = gsv[p][mt];
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
-        const int v = n * 4 + t;
+        // MP = 2: n-tiles [NT/2, NT) are the second member's vectors
+        const int h = (MP == 2 && n >= NT / 2) ? 1 : 0;
+        const int v = (n - h * (NT / 2)) * 4 + t;
         if (v < a.nv)
-          out[(size_t)v * a.out_vstride + (size_t)r * a.out_rstride + r + k] =
+          out[(size_t)h * a.out_mstride + (size_t)v * a.out_vstride + (size_t)r * a.out_rstride + r + k] =
               make_double2(acc[p][mt][n][0] * gs, acc[p][mt][n][1] * gs);
       }
     }
 }
 
 // One CTA per work item (grid: items x members).
-template <int NT, int LSPLIT>
+template <int NT, int LSPLIT, int MP = 1>
 __global__ void __launch_bounds__(kAnaWarps * 32)
 ana_kernel(PlanDev P, AnaArgs a) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) double smem[];
-  ana_item<NT, LSPLIT, false>(P, a, a.work[blockIdx.x], blockIdx.y, smem);
+  ana_item<NT, LSPLIT, false, MP>(P, a, a.work[blockIdx.x], blockIdx.y, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -910,6 +924,20 @@ ana_dfma_kernel(PlanDev P, AnaArgs a) {
 bool ana_dfma() {
   static const int knob = env_int("SWSDC_ANA_DFMA", 0);
   return knob != 0;
+}
+
+// Member pairs (a.nmembers pairs of members, a.nv <= 8 vectors each): one
+// CTA contracts both members' x with the same q tiles (NT = 4).
+template <int LSPLIT>
+int launch_ana_pairs_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st) {
+  const int warps = LSPLIT * ana_chunks_per_cta(LSPLIT);
+  const size_t smem = sizeof(double) * warps * ana_warp_doubles<4>();
+  auto kern = ana_kernel<4, LSPLIT, 2>;
+  SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
+  StageScope sc("legendre_analysis", st);
+  SW_CUDA(launch_pdl(kern, dim3(dim3(nwork, a.nmembers)), dim3(warps * 32), smem, st, P, a));
+  SW_LAUNCH_CHECK();
+  return kOk;
 }
 
 template <int NT, int LSPLIT>
@@ -1196,6 +1224,26 @@ int launch_analysis(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, c
   if (a.nv <= 16) return launch_ana_nt<4>(P, a, nwork, lsplit, st);
   set_error("analysis vectors per launch must be <= 16");
   return kUsage;
+}
+
+int launch_analysis_pairs(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, cudaStream_t st) {
+  if (a.nv <= 0) return kOk;
+  if (a.nv > 8) {
+    set_error("member-pair analysis takes <= 8 vectors per member");
+    return kUsage;
+  }
+  switch (lsplit) {
+    case 2: return launch_ana_pairs_t<2>(P, a, nwork, st);
+    case 3: return launch_ana_pairs_t<3>(P, a, nwork, st);
+    case 4: return launch_ana_pairs_t<4>(P, a, nwork, st);
+    default: return launch_ana_pairs_t<1>(P, a, nwork, st);
+  }
+}
+
+bool ana_pairs_ok(int nv, int nmembers) {
+  static const int knob = env_int("SWSDC_ANA_PAIRS", 1);
+  return knob != 0 && nv >= 1 && nv <= 8 && nmembers >= 2 && nmembers % 2 == 0 && !ana_dfma() &&
+         !ana_uses_tma(nv);
 }
 
 }  // namespace swsdc

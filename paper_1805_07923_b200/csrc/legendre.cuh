@@ -53,5 +53,9 @@ int ana_chunks_per_cta(int lsplit);
 int ana_ctas_per_sm(int nv, int lsplit);
 constexpr int kAnaSplits = 4;
 bool ana_uses_tma(int nv);
+// Ensemble analysis two members per CTA (a.nmembers = member pairs, nv <= 8
+// vectors each, members m and m + 1 adjacent at a.xl.mstride / a.out_mstride).
+bool ana_pairs_ok(int nv, int nmembers);
+int launch_analysis_pairs(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, cudaStream_t st);
 
 }  // namespace swsdc
