@@ -370,10 +370,8 @@ __global__ void SWSDC_REG_BOUNDS(K) f2g_reg_kernel(PlanDev P, const double2* eo,
   }
   __syncthreads();   // staging consumed; the rings reuse its space
   if (jhw < jh_end) {
-    swfft::ring_fft<K, true>(v, P.tw, lane, wst);
     double2* ring = rings + (size_t)warp * P.ring_stride;
-#pragma unroll
-    for (int m1 = 0; m1 < K; ++m1) ring[swfft::pad_idx(swfft::ring_out_index<K>(lane, m1))] = v[m1];
+    swfft::ring_fft_to<K, true>(v, P.tw, lane, wst, ring);
     if (RINGS) {
       __syncwarp();
       double2* dst = reinterpret_cast<double2*>(grid) + (size_t)f * grid_fstride + (size_t)jhw * P.I;
@@ -442,10 +440,7 @@ __global__ void SWSDC_REG_BOUNDS(K) g2f_reg_kernel(PlanDev P, const double* grid
     double2 v[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
-    swfft::ring_fft<K, false>(v, P.tw, lane, wst);
-    __syncwarp();
-#pragma unroll
-    for (int m1 = 0; m1 < K; ++m1) ring[swfft::pad_idx(swfft::ring_out_index<K>(lane, m1))] = v[m1];
+    swfft::ring_fft_to<K, false>(v, P.tw, lane, wst, ring);
   }
   __syncthreads();
   double* xf = x + (MODE == 0 ? 0 : (size_t)f * xl.mstride);
@@ -562,10 +557,7 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
       double2 v[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
-      swfft::ring_fft<K, true>(v, P.tw, lane, wst);
-      __syncwarp();
-#pragma unroll
-      for (int m1 = 0; m1 < K; ++m1) ring[swfft::pad_idx(swfft::ring_out_index<K>(lane, m1))] = v[m1];
+      swfft::ring_fft_to<K, true, K == 24>(v, P.tw, lane, wst, ring);
     }
   }
   __syncthreads();
@@ -598,10 +590,7 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
       double2 v[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
-      swfft::ring_fft<K, false>(v, P.tw, lane, wst);
-      __syncwarp();
-#pragma unroll
-      for (int m1 = 0; m1 < K; ++m1) ring[swfft::pad_idx(swfft::ring_out_index<K>(lane, m1))] = v[m1];
+      swfft::ring_fft_to<K, false, K == 24>(v, P.tw, lane, wst, ring);
     }
   }
   __syncthreads();
