@@ -412,6 +412,9 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
       ep[s] = std::sqrt(((double)s * s - (double)r * r) / (4.0 * s * s - 1.0));
     sect[r] = std::sqrt((2.0 * r + 3.0) / (2.0 * r + 2.0));
   }
+  // 1 / (s (s + 1)) for the psi / chi scaling of the SWE synthesis (-a ilap[s] = 1 / (a lambda_s))
+  std::vector<double> ilap(R + 66, 0.0);
+  for (int s = 1; s < R + 66; ++s) ilap[s] = 1.0 / ((double)s * (s + 1.0));
   std::vector<int> ck_off(R + 1);
   int nck = 0;
   for (int r = 0; r <= R; ++r) {
@@ -454,6 +457,7 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
   }
 
   int st = kOk;
+  double* d_ilap = nullptr;
   double *d_mu = nullptr, *d_w = nullptr, *d_beta = nullptr, *d_gsc = nullptr, *d_eps = nullptr,
          *d_a = nullptr, *d_b = nullptr, *d_sect = nullptr;
   int* d_off = nullptr;
@@ -461,7 +465,7 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
   double2* d_tw = nullptr;
   if ((st = upload(p, mu_n, &d_mu)) || (st = upload(p, w_n, &d_w)) ||
       (st = upload(p, beta, &d_beta)) || (st = upload(p, gsc, &d_gsc)) ||
-      (st = upload(p, eps, &d_eps)) || (st = upload(p, a, &d_a)) || (st = upload(p, b, &d_b)) ||
+      (st = upload(p, eps, &d_eps)) || (st = upload(p, ilap, &d_ilap)) || (st = upload(p, a, &d_a)) || (st = upload(p, b, &d_b)) ||
       (st = upload(p, sect, &d_sect)) || (st = upload(p, ck_off, &d_off)) ||
       (st = upload(p, tw, &d_tw)) || (st = upload(p, rev, &d_rev)) ||
       (st = upload_work(p, work))) {
@@ -487,6 +491,7 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
   P.beta = d_beta;
   P.gsc = d_gsc;
   P.eps = d_eps;
+  P.ilap = d_ilap;
   P.ck_off = d_off;
   P.tw = d_tw;
   P.rev = d_rev;

@@ -133,6 +133,7 @@ struct PlanDev {
   const double* beta;     // [(R+1) * ldk] scaled-recurrence coefficient beta[r][k], k = s - r
   const double* gsc;      // [(R+1) * ldk] scale g[r][k] relative to the chunk start
   const double* eps;      // [(R+1) * ldk] eps[r][s] = sqrt((s^2 - r^2) / (4 s^2 - 1)), index s
+  const double* ilap;     // [R + 66] 1 / (s (s + 1)) (s >= 1), 0 at s = 0: -a^2 / lambda_s / a^2
   const double2* ckpt;    // [sum_r nchunk(r)][Jh] (q_{s0}, q_{s0+1}) chunk seeds
   const int* ck_off;      // [R+1] first chunk index of row r in ckpt
   const double2* tw;      // [I] exp(-2 pi i e / I)

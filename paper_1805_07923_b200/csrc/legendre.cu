@@ -176,9 +176,12 @@ __device__ __forceinline__ double2 hfold(double2 hi, double2 lo, double e0, doub
 
 // Coefficients of the B synthesis fields at degree s = r + k0 + lane, scaled
 // by g, written to the warp's slab cs[b][lane].
-template <int B, int MODE>
+// TBL: 1 / (s (s + 1)) from the plan table (no division); measured faster in
+// the split (NSPLIT > 1) kernels, while in the NSPLIT = 1 kernel the divisions'
+// scheduling barrier keeps the register count (and occupancy) lower.
+template <int B, int MODE, bool TBL>
 __device__ __forceinline__ void stage_chunk(const ChunkRegs<B, MODE>& c, double2* cs, int r,
-                                            int s, double radius, int lane) {
+                                            int s, double radius, const double* ilap, int lane) {
   double2 v[B];
   if (MODE == kSynPlain) {
 #pragma unroll
@@ -190,9 +193,20 @@ __device__ __forceinline__ void stage_chunk(const ChunkRegs<B, MODE>& c, double2
     v[0] = make_double2(-r * c.raw[1].y - hp.x, r * c.raw[1].x - hp.y);
     v[1] = make_double2(-r * c.raw[0].y + hc.x, r * c.raw[0].x + hc.y);
   } else {
-    // psi = invlap(zeta), chi = invlap(delta) (swe.py:186-187), then 1/a (swe.py:189)
-    const double s0 = inv_lap_a(s, radius), sp = inv_lap_a(s + 1, radius),
-                 sm = inv_lap_a(s - 1, radius);
+    // psi = invlap(zeta), chi = invlap(delta) (swe.py:186-187), then 1/a (swe.py:189):
+    // (1 / lambda_s) / a = -a / (s (s + 1)), lambda_s = -s (s + 1) / a^2
+    // (spharm.py:321-333, s = 0 gauged to 0), from the plan table, no division
+    // (table read at staging time, not prefetched: it is tiny and L1-resident)
+    double s0, sp, sm;
+    if (TBL) {
+      s0 = -radius * ilap[s];
+      sp = -radius * ilap[s + 1];
+      sm = s >= 1 ? -radius * ilap[s - 1] : 0.0;
+    } else {
+      s0 = inv_lap_a(s, radius);
+      sp = inv_lap_a(s + 1, radius);
+      sm = inv_lap_a(s - 1, radius);
+    }
     const double2 hpsi = hfold(c.raw[2], c.raw[3], c.eps0, c.eps1, s, sp, sm);
     const double2 hchi = hfold(c.raw[4], c.raw[5], c.eps0, c.eps1, s, sp, sm);
     v[0] = make_double2(-r * c.raw[1].y * s0 - hpsi.x, r * c.raw[1].x * s0 - hpsi.y);  // U/a
@@ -293,7 +307,7 @@ syn_kernel(PlanDev P, SynArgs a) {
       load_chunk<B, MODE>(nx, P, a, r, c0, nstep, lane, jh, off_r);
       for (int ci = c0; ci < c1; ++ci) {
         __syncwarp();
-        stage_chunk<B, MODE>(nx, cs, r, r + ci * kChunk + lane, a.radius, lane);
+        stage_chunk<B, MODE, (NSPLIT > 1)>(nx, cs, r, r + ci * kChunk + lane, a.radius, P.ilap, lane);
         bs[lane] = nx.beta;
         if (lane < 2) bs[kChunk + lane] = nx.beta_x;
         double qa[kSynNL], qb[kSynNL];
