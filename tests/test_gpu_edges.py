@@ -80,8 +80,10 @@ def test_batch_sizes_match_oracle(batch):
     assert rel_err(back, np.stack([oplan.analyze(gi) for gi in want])) < TOL
 
 
-@pytest.mark.parametrize("members", [2, 5, 17])
+@pytest.mark.parametrize("members", [2, 4, 5, 17, 64])
 def test_batched_eval_fe_equals_per_member(members):
+    """Even member counts take the member-pair analysis (two members per CTA
+    sharing the q tiles), odd ones the per-member kernel."""
     from paper_1805_07923_b200 import swe
     rng = np.random.default_rng(members)
     R = 21
@@ -152,3 +154,20 @@ def test_spec_combine_multi_equals_single_launches():
     outs = swe.spec_combine_multi(many, 15)
     ref = swe.spec_combine([1.0, 1.0], [xs[0], xs[2]], 15)
     assert all(torch.equal(o, ref) for o in outs)
+
+
+@pytest.mark.parametrize("batch", [2, 3, 6])
+def test_batched_div_curl_equals_per_member(batch):
+    """analyze_vector_div_curl over a batch (4 analysis vectors per member: the
+    member-pair path for even batches) equals the per-member calls."""
+    rng = np.random.default_rng(100 + batch)
+    R = 31
+    plan, _ = _plans(R)
+    c = _rand_coeffs(rng, R, 2 * batch)
+    u = plan.synthesize(torch.as_tensor(c[:batch]).cuda())
+    v = plan.synthesize(torch.as_tensor(c[batch:]).cuda())
+    d, k = plan.analyze_vector_div_curl(u, v)
+    for b in range(batch):
+        d1, k1 = plan.analyze_vector_div_curl(u[b], v[b])
+        assert rel_err(d[b].cpu().numpy(), d1.cpu().numpy()) < 1e-12
+        assert rel_err(k[b].cpu().numpy(), k1.cpu().numpy()) < 1e-12
