@@ -549,9 +549,18 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
       const int k = k0 + p + 2 * (8 * mt + g);
       gsv[p][mt] = (active && k < nout) ? P.gsc[(size_t)r * P.ldk + k] : 0.0;
     }
+  // first-block seed and mu of this lane's latitude, loaded together with the
+  // betas (one round trip for all the item's table loads; the recurrence of
+  // each later block is seeded one block ahead)
+  const double2* seeds = P.ckpt + (size_t)(wk.z + (c - wk.y)) * P.Jh;
+  double2 sd_nx = make_double2(0.0, 0.0);
+  double mu_nx = 0.0;
+  if (active) {
+    const int jh0 = (half << 5) + lane;
+    if (jh0 < P.Jh) { sd_nx = seeds[jh0]; mu_nx = P.mu_n[jh0]; }
+  }
   if (active) {
     bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
-    const double2* seeds = P.ckpt + (size_t)(wk.z + (c - wk.y)) * P.Jh;
     const int nc = a.xl.nc, jh4 = a.xl.jh4;
     const double* xr = x + (size_t)r * jh4 * 2 * nc * 4;
     const int nblk = (P.Jh + 31) >> 5;
@@ -608,13 +617,6 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
     };
 #pragma unroll
     for (int d = 0; d < kBDepth - 1; ++d) issue_next();
-    // seed and mu of this lane's latitude in the next block, fetched one block ahead
-    double2 sd_nx = make_double2(0.0, 0.0);
-    double mu_nx = 0.0;
-    {
-      const int jh0 = (half << 5) + lane;
-      if (jh0 < P.Jh) { sd_nx = seeds[jh0]; mu_nx = P.mu_n[jh0]; }
-    }
     int ks = 0;
     // a row's last chunk with <= 16 degrees has an empty upper m-tile (degrees
     // 16..31 of the chunk): its warps run an instantiation without those DMMAs
