@@ -32,6 +32,19 @@
 #include "legendre.cuh"
 
 namespace swsdc {
+#ifdef ANA_TRACE
+// debug build only (tools/ana_trace.py): per-warp %globaltimer stamps of the
+// analysis phases, read back with swsdc_debug_ana_trace
+__device__ unsigned long long g_ana_trace[16384][8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define ANA_STAMP(k) do { if ((threadIdx.x & 31) == 0) { const int wid_ = (blockIdx.y * gridDim.x + blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); if (wid_ < 16384) g_ana_trace[wid_][k] = gtime(); } } while (0)
+#else
+#define ANA_STAMP(k) do {} while (0)
+#endif
 
 // ---------------------------------------------------------------------------
 // Checkpoint seeds: the reference recurrence (spharm.py:153-169) evaluated
@@ -522,6 +535,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
   double2* out = a.out + (size_t)(MP * m) * a.out_mstride;
   const int r = wk.x, c = wk.y + warp / LSPLIT, half = warp % LSPLIT;
   const int nout = a.smax - r + 1;
+  ANA_STAMP(0);
 
   if (a.zero_fill && wk.y == 0) {
 #pragma unroll
@@ -615,6 +629,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
       ijb += blk ? (LSPLIT - 1) * 8 + 1 : 1;
       ip += blk ? jump : jb_stride;
     };
+    ANA_STAMP(1);
 #pragma unroll
     for (int d = 0; d < kBDepth - 1; ++d) issue_next();
     int ks = 0;
@@ -649,6 +664,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
         for (int kk = 0; kk < kChunk; ++kk) qs[((kk & 1) * 16 + (kk >> 1)) * kQS + lane] = 0.0;
       }
       __syncwarp();
+      if (jb32 == half) ANA_STAMP(2);
       // k-steps of this block; blocks reaching past Jh (padding rows of x may
       // hold non-finite bits, q = 0 there) take the masked instantiation
       auto ksteps = [&](auto full_c) {
@@ -658,6 +674,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
           issue_next();
           cp_async_wait<kBDepth - 1>();
           __syncwarp();
+          if (ks == 0) ANA_STAMP(3);
           // no column mask: column n of D depends only on column n of B, and
           // columns >= 2 nv only feed accumulators that are never written
           const double* bsrc = bring + (ks & (kBDepth - 1)) * (2 * NT * 32);
@@ -689,6 +706,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
     else blocks(std::integral_constant<int, 2>());
     cp_async_wait<0>();
   }
+  ANA_STAMP(4);
 
   if (LSPLIT > 1) {
     // warps half > 0 hand their partial sums to the half-0 warp of their chunk;
@@ -732,6 +750,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
     return;
   }
 
+  ANA_STAMP(5);
   // epilogue: row k = k0 + p + 2 (8 mt + g); columns (re, im) of vector n*4 + t
 #pragma unroll
   for (int p = 0; p < 2; ++p)
@@ -750,6 +769,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
               make_double2(acc[p][mt][n][0] * gs, acc[p][mt][n][1] * gs);
       }
     }
+  ANA_STAMP(6);
 }
 
 // One CTA per work item (grid: items x members).
@@ -1263,3 +1283,14 @@ bool ana_pairs_ok(int nv, int nmembers) {
 }
 
 }  // namespace swsdc
+
+#ifdef ANA_TRACE
+extern "C" int swsdc_debug_ana_trace(unsigned long long* host, int clear) {
+  if (clear) {
+    static unsigned long long zero[16384][8];
+    return cudaMemcpyToSymbol(swsdc::g_ana_trace, zero, sizeof(zero)) == cudaSuccess ? 0 : 3;
+  }
+  return cudaMemcpyFromSymbol(host, swsdc::g_ana_trace, sizeof(unsigned long long) * 16384 * 8) ==
+                 cudaSuccess ? 0 : 3;
+}
+#endif
