@@ -34,6 +34,19 @@
 
 namespace swsdc {
 namespace cg = cooperative_groups;
+#ifdef GRID_TRACE
+// debug build only (tools/grid_trace.py): per-CTA %globaltimer stamps of the
+// fused F_E grid kernel's phases, read back with swsdc_debug_grid_trace
+__device__ unsigned long long g_grid_trace[16384][8];
+__device__ __forceinline__ unsigned long long gtime_g() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GRID_STAMP(k) do { if (threadIdx.x == 0) { const int cid_ = blockIdx.y * gridDim.x + blockIdx.x; if (cid_ < 16384) g_grid_trace[cid_][k] = gtime_g(); } } while (0)
+#else
+#define GRID_STAMP(k) do {} while (0)
+#endif
 namespace {
 
 constexpr int kSweMaxPts = 4;   // grid points per thread in the fused SWE kernel
@@ -547,8 +560,10 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
   const int RS = P.ring_stride;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const size_t fstride = (size_t)(P.R + 1) * P.Jh * 2;
+  GRID_STAMP(0);
   fill_rings(rings, P, eo + (size_t)m * eo_mstride + (size_t)jh * 2, fstride, NIN, 1, 0, 0, true);
   __syncthreads();
+  GRID_STAMP(1);
   {
     double2 wst[3];
     swfft::cross_twiddles<K, true>(wst, P.tw, lane);
@@ -561,6 +576,7 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
     }
   }
   __syncthreads();
+  GRID_STAMP(2);
   const double mu = P.mu_n[jh];
   const double fn = 2.0 * omega * mu;         // f = 2 Omega mu (swe.py:178); south: -fn
   const double c2o = 2.0 * omega / radius;    // swe.py:179
@@ -582,6 +598,7 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
     }
   }
   __syncthreads();
+  GRID_STAMP(3);
   {
     double2 wst[3];
     swfft::cross_twiddles<K, false>(wst, P.tw, lane);
@@ -594,12 +611,14 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
     }
   }
   __syncthreads();
+  GRID_STAMP(4);
   if constexpr (!CL) {
     const double w = P.w_n[jh];
     swe_grid_output<NONLIN>(rings, P, x + (size_t)m * xl.mstride, xl, jh, w, w * ic2, 1.0 / radius);
   } else {
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
+    GRID_STAMP(5);
     const int c = (int)cl.block_rank();
     const int jb0 = jh - c;                  // first latitude pair of this cluster's block
     const int nr = P.R + 1, r_lo = c * nr / 4, r_hi = (c + 1) * nr / 4;
@@ -613,11 +632,13 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
       swe_out_one<NONLIN>(ri, P, xm, xl, r, jhi, wi, wi / (1.0 - mui * mui), ia,
                           jn_of(P, jhi) == js_of(P, jhi));
     }
+    GRID_STAMP(6);
     // only the remote shared-memory reads above must be complete before a CTA
     // may exit, and they are (their values were consumed): a relaxed arrive
     // does not wait for this CTA's outstanding x stores as cl.sync()'s release would
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+    GRID_STAMP(7);
   }
 }
 
@@ -1299,3 +1320,14 @@ int launch_swe_grid(const PlanDev& P, bool nonlinear, const double2* eo, long lo
 }
 
 }  // namespace swsdc
+
+#ifdef GRID_TRACE
+extern "C" int swsdc_debug_grid_trace(unsigned long long* host, int clear) {
+  if (clear) {
+    static unsigned long long zero[16384][8];
+    return cudaMemcpyToSymbol(swsdc::g_grid_trace, zero, sizeof(zero)) == cudaSuccess ? 0 : 3;
+  }
+  return cudaMemcpyFromSymbol(host, swsdc::g_grid_trace, sizeof(unsigned long long) * 16384 * 8) ==
+                 cudaSuccess ? 0 : 3;
+}
+#endif
