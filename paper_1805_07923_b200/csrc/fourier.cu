@@ -106,6 +106,48 @@ __device__ __forceinline__ void pair_spectrum(double2 E, double2 O, int r, doubl
 // (E, O) rows eo[q][r][jh0 + i]; every slot is written (zeros off-band).
 // Loads are issued kU at a time before use so each thread keeps several
 // global reads in flight.
+// One pair (np = 1, natural order), NR rings: thread t takes the rows
+// r = t, t + nt, ... of every field -- no index division -- with all its
+// loads in flight before the spectra are formed.
+template <int NR>
+__device__ __forceinline__ void fill_rings_pair(double2* rings, const PlanDev& P, const double2* eo,
+                                                size_t fstride) {
+  const int R = P.R, I = P.I, RS = P.ring_stride, nt = blockDim.x;
+  for (int r0 = threadIdx.x; r0 <= R; r0 += 2 * nt) {
+    double2 E[2][NR], O[2][NR];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = r0 + h * nt;
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        E[h][q] = O[h][q] = d2(0.0, 0.0);
+        if (r <= R) {
+          const double2* src = eo + q * fstride + (size_t)r * P.Jh * 2;
+          E[h][q] = src[0];
+          O[h][q] = src[1];
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = r0 + h * nt;
+      if (r <= R) {
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          double2 zp, zm;
+          pair_spectrum(E[h][q], O[h][q], r, zp, zm);
+          double2* ring = rings + (size_t)q * RS;
+          ring[swfft::pad_idx(r)] = zp;
+          if (r != 0) ring[swfft::pad_idx(I - r)] = zm;
+        }
+      }
+    }
+  }
+  for (int k = R + 1 + threadIdx.x; k < I - R; k += nt)
+#pragma unroll
+    for (int q = 0; q < NR; ++q) rings[(size_t)q * RS + swfft::pad_idx(k)] = d2(0.0, 0.0);
+}
+
 __device__ __forceinline__ void fill_rings(double2* rings, const PlanDev& P, const double2* eo,
                                            size_t fstride, int nr, int np, int lnp, int jh0,
                                            bool natural = false) {
@@ -561,7 +603,7 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const size_t fstride = (size_t)(P.R + 1) * P.Jh * 2;
   GRID_STAMP(0);
-  fill_rings(rings, P, eo + (size_t)m * eo_mstride + (size_t)jh * 2, fstride, NIN, 1, 0, 0, true);
+  fill_rings_pair<NIN>(rings, P, eo + (size_t)m * eo_mstride + (size_t)jh * 2, fstride);
   __syncthreads();
   GRID_STAMP(1);
   {
