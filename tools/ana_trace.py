@@ -1,6 +1,5 @@
 """Phase timeline of the DMMA analysis kernel at config 1 from a trace build of
 legendre.cu (nvcc ... -DANA_TRACE, linked as abtest/lib_trace.so, used via SWSDC_LIB):
-(-DANA_TRACE, abtest/lib_trace.so via SWSDC_LIB): per-warp %globaltimer
 stamps 0 entry, 1 tables loaded, 2 first q tile done, 3 first x fragments
 arrived, 4 k-loop done, 5 reduction done, 6 epilogue stored."""
 import ctypes, os, sys
