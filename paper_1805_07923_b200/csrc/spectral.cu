@@ -41,45 +41,42 @@ __device__ __forceinline__ double2 hshift(const double2* Yv, const double* eps_r
   return out;
 }
 
+// Grid (s blocks, R + 1 rows, members): one row (m, r) per y/z coordinate,
+// degrees s across x -- no per-element index division.
 __global__ void finalize_swe_kernel(PlanDev P, const double2* Y, long long y_mstride, int ldy,
                                     double2* out, long long out_mstride, int nonlin,
                                     double radius, int nmembers, RowFilter rf) {
   pdl_wait();
   pdl_trigger();
   const int R = P.R;
-  const long long total = (long long)nmembers * (R + 1) * (R + 1);
+  const int s = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y, m = blockIdx.z;
+  if (s > R || r % rf.mod != rf.rank) return;
+  (void)nmembers;
   const long long plane = (long long)(R + 1) * (R + 1);
   const long long ystride_v = (long long)(R + 1) * ldy;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int m = (int)(idx / plane);
-    const int rs = (int)(idx - m * plane);
-    const int r = rs / (R + 1), s = rs - r * (R + 1);
-    if (r % rf.mod != rf.rank) continue;
-    double2* o = out + m * out_mstride + rs;
-    double2 phi = make_double2(0.0, 0.0), zeta = phi, delta = phi;
-    if (s >= r) {
-      const double2* Ym = Y + m * y_mstride + (long long)r * ldy;
-      const double* eps_r = P.eps + (size_t)r * P.ldk;
-      if (nonlin) {
-        const double2 h0 = hshift(Ym + 4 * ystride_v, eps_r, r, s);
-        const double2 h1 = hshift(Ym + 5 * ystride_v, eps_r, r, s);
-        const double2 h2 = hshift(Ym + 6 * ystride_v, eps_r, r, s);
-        const double2 p0 = Ym[s], p1 = Ym[ystride_v + s], p2 = Ym[2 * ystride_v + s];
-        const double2 ke = Ym[3 * ystride_v + s];
-        const double lam = lam_of(s, radius);
-        phi = make_double2(p0.x + h0.x, p0.y + h0.y);
-        zeta = make_double2(p1.x + h1.x, p1.y + h1.y);
-        delta = make_double2(p2.x + h2.x - lam * ke.x, p2.y + h2.y - lam * ke.y);
-      } else {
-        zeta = Ym[s];
-        delta = Ym[ystride_v + s];
-      }
+  double2* o = out + m * out_mstride + (long long)r * (R + 1) + s;
+  double2 phi = make_double2(0.0, 0.0), zeta = phi, delta = phi;
+  if (s >= r) {
+    const double2* Ym = Y + m * y_mstride + (long long)r * ldy;
+    const double* eps_r = P.eps + (size_t)r * P.ldk;
+    if (nonlin) {
+      const double2 h0 = hshift(Ym + 4 * ystride_v, eps_r, r, s);
+      const double2 h1 = hshift(Ym + 5 * ystride_v, eps_r, r, s);
+      const double2 h2 = hshift(Ym + 6 * ystride_v, eps_r, r, s);
+      const double2 p0 = Ym[s], p1 = Ym[ystride_v + s], p2 = Ym[2 * ystride_v + s];
+      const double2 ke = Ym[3 * ystride_v + s];
+      const double lam = lam_of(s, radius);
+      phi = make_double2(p0.x + h0.x, p0.y + h0.y);
+      zeta = make_double2(p1.x + h1.x, p1.y + h1.y);
+      delta = make_double2(p2.x + h2.x - lam * ke.x, p2.y + h2.y - lam * ke.y);
+    } else {
+      zeta = Ym[s];
+      delta = Ym[ystride_v + s];
     }
-    o[0] = phi;
-    o[plane] = zeta;
-    o[2 * plane] = delta;
   }
+  o[0] = phi;
+  o[plane] = zeta;
+  o[2 * plane] = delta;
 }
 
 __global__ void finalize_divcurl_kernel(PlanDev P, const double2* Y, long long y_mstride, int ldy,
@@ -309,54 +306,51 @@ __global__ void spec_combine_kernel(SpecCombineArgs a, long long nmat, RowFilter
   }
 }
 
-// b = sum_k w_k x_k -> theta = (I - beta F_I)^-1 b -> fi = L_G(theta)
+// b = sum_k w_k x_k -> theta = (I - beta F_I)^-1 b -> fi = L_G(theta).
+// Grid (s blocks, R + 1 rows, states): one row per y/z coordinate.
 __global__ void sweep_node_kernel(int R, ModelConsts c, double beta, SpecCombineArgs a,
                                   double2* theta, double2* fi, long long nstates, RowFilter rf) {
   pdl_wait();
   pdl_trigger();
+  const int s = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+  const long long m = blockIdx.z;
+  if (s > R || r % rf.mod != rf.rank) return;
+  (void)nstates;
   const long long plane = (long long)(R + 1) * (R + 1);
-  const long long total = nstates * plane;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long m = idx / plane;
-    const int rs = (int)(idx - m * plane);
-    const int r = rs / (R + 1), s = rs - r * (R + 1);
-    if (r % rf.mod != rf.rank) continue;
-    const long long o = m * 3 * plane + rs;
-    if (s < r) {
-      // structurally zero coefficients (spharm.py:6-10): zeros out, no term reads
-      const double2 z = make_double2(0.0, 0.0);
-      theta[o] = z; theta[o + plane] = z; theta[o + 2 * plane] = z;
-      fi[o] = z; fi[o + plane] = z; fi[o + 2 * plane] = z;
-      continue;
-    }
-    double2 b[3];
-#pragma unroll
-    for (int f = 0; f < 3; ++f) b[f] = make_double2(0.0, 0.0);
-    for (int k = 0; k < a.n; ++k) {
-#pragma unroll
-      for (int f = 0; f < 3; ++f) {
-        const double2 v = a.x[k][o + f * plane];
-        b[f].x = fma(a.w[k], v.x, b[f].x);
-        b[f].y = fma(a.w[k], v.y, b[f].y);
-      }
-    }
-    const double lam = lam_of(s, c.radius);
-    const double d = 1.0 - beta * c.nu * lam;
-    const double det = d * d - beta * beta * lam * c.phi_bar;
-    const double id = 1.0 / det;
-    const double bp = beta * c.phi_bar, bl = beta * lam;
-    const double2 ph = make_double2((d * b[0].x - bp * b[2].x) * id, (d * b[0].y - bp * b[2].y) * id);
-    const double2 ze = make_double2(b[1].x / d, b[1].y / d);
-    const double2 de = make_double2((d * b[2].x - bl * b[0].x) * id, (d * b[2].y - bl * b[0].y) * id);
-    theta[o] = ph;
-    theta[o + plane] = ze;
-    theta[o + 2 * plane] = de;
-    const double nl = c.nu * lam;
-    fi[o] = make_double2(-c.phi_bar * de.x + nl * ph.x, -c.phi_bar * de.y + nl * ph.y);
-    fi[o + plane] = make_double2(nl * ze.x, nl * ze.y);
-    fi[o + 2 * plane] = make_double2(-lam * ph.x + nl * de.x, -lam * ph.y + nl * de.y);
+  const long long o = m * 3 * plane + (long long)r * (R + 1) + s;
+  if (s < r) {
+    // structurally zero coefficients (spharm.py:6-10): zeros out, no term reads
+    const double2 z = make_double2(0.0, 0.0);
+    theta[o] = z; theta[o + plane] = z; theta[o + 2 * plane] = z;
+    fi[o] = z; fi[o + plane] = z; fi[o + 2 * plane] = z;
+    return;
   }
+  double2 b[3];
+#pragma unroll
+  for (int f = 0; f < 3; ++f) b[f] = make_double2(0.0, 0.0);
+  for (int k = 0; k < a.n; ++k) {
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      const double2 v = a.x[k][o + f * plane];
+      b[f].x = fma(a.w[k], v.x, b[f].x);
+      b[f].y = fma(a.w[k], v.y, b[f].y);
+    }
+  }
+  const double lam = lam_of(s, c.radius);
+  const double d = 1.0 - beta * c.nu * lam;
+  const double det = d * d - beta * beta * lam * c.phi_bar;
+  const double id = 1.0 / det;
+  const double bp = beta * c.phi_bar, bl = beta * lam;
+  const double2 ph = make_double2((d * b[0].x - bp * b[2].x) * id, (d * b[0].y - bp * b[2].y) * id);
+  const double2 ze = make_double2(b[1].x / d, b[1].y / d);
+  const double2 de = make_double2((d * b[2].x - bl * b[0].x) * id, (d * b[2].y - bl * b[0].y) * id);
+  theta[o] = ph;
+  theta[o + plane] = ze;
+  theta[o + 2 * plane] = de;
+  const double nl = c.nu * lam;
+  fi[o] = make_double2(-c.phi_bar * de.x + nl * ph.x, -c.phi_bar * de.y + nl * ph.y);
+  fi[o + plane] = make_double2(nl * ze.x, nl * ze.y);
+  fi[o + 2 * plane] = make_double2(-lam * ph.x + nl * de.x, -lam * ph.y + nl * de.y);
 }
 
 int grid_for(long long n, int threads) {
@@ -371,9 +365,10 @@ int grid_for(long long n, int threads) {
 int launch_finalize_swe(const PlanDev& P, const double2* Y, long long y_mstride, int ldy,
                         double2* out, long long out_mstride, bool nonlin, double radius,
                         int nmembers, cudaStream_t st, RowFilter rf) {
-  const long long n = (long long)nmembers * (P.R + 1) * (P.R + 1);
+  const int tx = P.R + 1 >= 128 ? 128 : 64;
+  const dim3 grid((P.R + 1 + tx - 1) / tx, P.R + 1, nmembers);
   StageScope sc("finalize_swe", st);
-  SW_CUDA(launch_pdl(finalize_swe_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, P, Y, y_mstride, ldy, out, out_mstride, nonlin ? 1 : 0, radius, nmembers, rf));
+  SW_CUDA(launch_pdl(finalize_swe_kernel, grid, dim3(tx), 0, st, P, Y, y_mstride, ldy, out, out_mstride, nonlin ? 1 : 0, radius, nmembers, rf));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -449,9 +444,10 @@ int launch_spec_combine(const SpecCombineArgs& a, long long nmat, cudaStream_t s
 
 int launch_sweep_node(int R, const ModelConsts& c, double beta, const SpecCombineArgs& a,
                       double2* theta, double2* fi, long long nstates, cudaStream_t st) {
-  const long long n = nstates * (R + 1) * (R + 1);
+  const int tx = R + 1 >= 128 ? 128 : 64;
+  const dim3 grid((R + 1 + tx - 1) / tx, R + 1, (unsigned)nstates);
   StageScope sc("sweep_node", st);
-  SW_CUDA(launch_pdl(sweep_node_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, R, c, beta, a, theta, fi, nstates, current_row_filter()));
+  SW_CUDA(launch_pdl(sweep_node_kernel, grid, dim3(tx), 0, st, R, c, beta, a, theta, fi, nstates, current_row_filter()));
   SW_LAUNCH_CHECK();
   return kOk;
 }
