@@ -108,30 +108,28 @@ __global__ void finalize_divcurl_kernel(PlanDev P, const double2* Y, long long y
 }
 
 // state layout: [m][3][R+1][R+1] complex, fields (phi', zeta, delta)
+// Grid (s blocks, R + 1 rows, states).
 __global__ void eval_fi_kernel(int R, ModelConsts c, const double2* x, double2* out,
                                long long nmat, RowFilter rf) {
   pdl_wait();
   pdl_trigger();
+  const int s = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+  const long long m = blockIdx.z;
+  if (s > R || r % rf.mod != rf.rank) return;
+  (void)nmat;
   const long long plane = (long long)(R + 1) * (R + 1);
-  const long long total = nmat * plane;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long m = idx / plane;
-    const int rs = (int)(idx - m * plane);
-    const int r = rs / (R + 1), s = rs - r * (R + 1);
-    if (r % rf.mod != rf.rank) continue;
-    const double lam = lam_of(s, c.radius);
-    const double nl = c.nu * lam;
-    const double2* xm = x + m * 3 * plane + rs;
-    double2* om = out + m * 3 * plane + rs;
-    const double2 z0 = make_double2(0.0, 0.0);
-    // s < r: structurally zero input (spharm.py:6-10), not read
-    const bool up = s >= r;
-    const double2 ph = up ? xm[0] : z0, ze = up ? xm[plane] : z0, de = up ? xm[2 * plane] : z0;
-    om[0] = make_double2(-c.phi_bar * de.x + nl * ph.x, -c.phi_bar * de.y + nl * ph.y);
-    om[plane] = make_double2(nl * ze.x, nl * ze.y);
-    om[2 * plane] = make_double2(-lam * ph.x + nl * de.x, -lam * ph.y + nl * de.y);
-  }
+  const long long rs = (long long)r * (R + 1) + s;
+  const double lam = lam_of(s, c.radius);
+  const double nl = c.nu * lam;
+  const double2* xm = x + m * 3 * plane + rs;
+  double2* om = out + m * 3 * plane + rs;
+  const double2 z0 = make_double2(0.0, 0.0);
+  // s < r: structurally zero input (spharm.py:6-10), not read
+  const bool up = s >= r;
+  const double2 ph = up ? xm[0] : z0, ze = up ? xm[plane] : z0, de = up ? xm[2 * plane] : z0;
+  om[0] = make_double2(-c.phi_bar * de.x + nl * ph.x, -c.phi_bar * de.y + nl * ph.y);
+  om[plane] = make_double2(nl * ze.x, nl * ze.y);
+  om[2 * plane] = make_double2(-lam * ph.x + nl * de.x, -lam * ph.y + nl * de.y);
 }
 
 __global__ void solve_kernel(int R, ModelConsts c, double beta, const double2* b, double2* out,
@@ -365,6 +363,7 @@ int grid_for(long long n, int threads) {
 int launch_finalize_swe(const PlanDev& P, const double2* Y, long long y_mstride, int ldy,
                         double2* out, long long out_mstride, bool nonlin, double radius,
                         int nmembers, cudaStream_t st, RowFilter rf) {
+  if (nmembers <= 0) return kOk;
   const int tx = P.R + 1 >= 128 ? 128 : 64;
   const dim3 grid((P.R + 1 + tx - 1) / tx, P.R + 1, nmembers);
   StageScope sc("finalize_swe", st);
@@ -384,9 +383,11 @@ int launch_finalize_divcurl(const PlanDev& P, const double2* Y, long long y_mstr
 
 int launch_eval_fi(int R, const ModelConsts& c, const double2* x, double2* out, long long nmat,
                    cudaStream_t st) {
-  const long long n = nmat * (R + 1) * (R + 1);
+  if (nmat <= 0) return kOk;
+  const int tx = R + 1 >= 128 ? 128 : 64;
+  const dim3 grid((R + 1 + tx - 1) / tx, R + 1, (unsigned)nmat);
   StageScope sc("eval_fi", st);
-  SW_CUDA(launch_pdl(eval_fi_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, R, c, x, out, nmat, current_row_filter()));
+  SW_CUDA(launch_pdl(eval_fi_kernel, grid, dim3(tx), 0, st, R, c, x, out, nmat, current_row_filter()));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -444,6 +445,7 @@ int launch_spec_combine(const SpecCombineArgs& a, long long nmat, cudaStream_t s
 
 int launch_sweep_node(int R, const ModelConsts& c, double beta, const SpecCombineArgs& a,
                       double2* theta, double2* fi, long long nstates, cudaStream_t st) {
+  if (nstates <= 0) return kOk;
   const int tx = R + 1 >= 128 ? 128 : 64;
   const dim3 grid((R + 1 + tx - 1) / tx, R + 1, (unsigned)nstates);
   StageScope sc("sweep_node", st);
