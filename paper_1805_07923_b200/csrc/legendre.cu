@@ -511,16 +511,14 @@ __host__ __device__ constexpr int ana_warp_doubles() {
   return kChunk * kQS + kChunk + kBDepth * 2 * NT * 32;
 }
 
-// One work item (r, first chunk, checkpoint index) of member m.  PERSIST: the
-// CTA continues with another item afterwards, so the warps of a chunk meet
-// once more after the split reduction (the half-0 warp reads the other warps'
-// shared memory, which their next item overwrites).  A persistent grid walking
-// the item list was measured (profiles/r01/experiments.md) and not kept.
+// One work item (r, first chunk, checkpoint index) of member m (one CTA; a
+// persistent grid walking the item list was measured in
+// profiles/r01/experiments.md and not kept).
 // MP = 2: members 2m and 2m + 1 of an ensemble share the CTA -- n-tiles
 // [0, NT/2) come from the first member's x, [NT/2, NT) from the second's
 // (each member's layout holds NT/2 n-tiles, a.nv <= 4 NT/2 vectors) -- so the
 // q tile and the A fragments serve twice the columns.
-template <int NT, int LSPLIT, bool PERSIST, int MP = 1>
+template <int NT, int LSPLIT, int MP = 1>
 __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, const int4 wk, int m,
                                          double* smem) {
   static_assert(MP == 1 || (MP == 2 && NT % 4 == 0), "member pairs need NT / 2 even");
@@ -728,10 +726,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
     }
     asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
     if (!active) return;
-    if (half > 0) {
-      if (PERSIST) asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
-      return;
-    }
+    if (half > 0) return;
     for (int h = 1; h < LSPLIT; ++h) {
       const double* src = smem + (size_t)(warp + h) * ana_warp_doubles<NT>();
 #pragma unroll
@@ -745,7 +740,6 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
             acc[p][mt][n][1] += src[(e + 1) * 32 + lane];
           }
     }
-    if (PERSIST) asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
   } else if (!active) {
     return;
   }
@@ -779,7 +773,7 @@ ana_kernel(PlanDev P, AnaArgs a) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) double smem[];
-  ana_item<NT, LSPLIT, false, MP>(P, a, a.work[blockIdx.x], blockIdx.y, smem);
+  ana_item<NT, LSPLIT, MP>(P, a, a.work[blockIdx.x], blockIdx.y, smem);
 }
 
 // ---------------------------------------------------------------------------
