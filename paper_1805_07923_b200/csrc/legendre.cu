@@ -369,24 +369,38 @@ syn_kernel(PlanDev P, SynArgs a) {
     }
   }
   if (NSPLIT > 1) {
-    // deterministic reduction of the warps' partial rows (fixed warp order)
+    // deterministic reduction of the warps' partial rows (fixed warp order),
+    // per row: a row owned by one warp is written straight out; the warps of
+    // a shared row meet at a named barrier of their own (1 + row) and split
+    // the summation, so neither waits for the other row's warps
+    const int wb = wrow == 0 ? 0 : w1, we = wrow == 0 ? w1 : NSPLIT;
+    const int nrw = we - wb;
+    const int r = rows[wrow];
+    if (nrw == 1) {
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+#pragma unroll
+        for (int l = 0; l < kSynNL; ++l)
+          if (jh[l] < P.Jh) {
+            double2* o = a.eo + (((size_t)b * (P.R + 1) + r) * P.Jh + jh[l]) * 2;
+            o[0] = E[b][l];
+            o[1] = O[b][l];
+          }
+      return;
+    }
     flush_row<B>(E, O, red + (size_t)warp * B * kSynLat * 2, lane);
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < 2 * B * kSynLat; idx += blockDim.x) {
-      const int ir = idx / (B * kSynLat);
-      const int rem = idx - ir * B * kSynLat;
-      const int b = rem / kSynLat, lj = rem - b * kSynLat;
-      if (ir == 1 && !two) continue;
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + wrow), "r"(32 * nrw) : "memory");
+    for (int idx = (warp - wb) * 32 + lane; idx < B * kSynLat; idx += 32 * nrw) {
+      const int b = idx / kSynLat, lj = idx - b * kSynLat;
       const int j = lg * kSynLat + lj;
       if (j >= P.Jh) continue;
       double2 e = make_double2(0.0, 0.0), o = e;
-      const int wb = ir == 0 ? 0 : w1, we = ir == 0 ? w1 : NSPLIT;   // the row's warps
       for (int w = wb; w < we; ++w) {
         const double2* src = red + ((size_t)w * B * kSynLat + (size_t)b * kSynLat + lj) * 2;
         e.x += src[0].x; e.y += src[0].y;
         o.x += src[1].x; o.y += src[1].y;
       }
-      double2* dst = a.eo + (((size_t)b * (P.R + 1) + rows[ir]) * P.Jh + j) * 2;
+      double2* dst = a.eo + (((size_t)b * (P.R + 1) + r) * P.Jh + j) * 2;
       dst[0] = e;
       dst[1] = o;
     }
