@@ -229,6 +229,12 @@ int pick_ana_split(int nch, int nmembers, int nv, int Jh) {
   }
   const int nblk = (Jh + 31) / 32;
   const double useful = (double)nch * nmembers * nblk;
+  // Problems spanning several waves even unsplit gain nothing from the split
+  // but pay its per-item cost (seeds, split reduction, epilogue: ~1 latitude
+  // block of k-steps, tools/ana_trace.py): charge it there (T1279: 19.06 ->
+  // 18.33 ms per config-3 step); small problems keep the wave-fitting choice.
+  const long long slots1 = (long long)sms * ana_ctas_per_sm(nv, 1) * ana_chunks_per_cta(1);
+  const double item_cost = (long long)nch * nmembers >= 2 * slots1 ? 1.0 : 0.0;
   int best = 1;
   double best_eff = -1.0;
   for (int ls = 1; ls <= kAnaSplits; ++ls) {
@@ -237,7 +243,7 @@ int pick_ana_split(int nch, int nmembers, int nv, int Jh) {
     const long long slots = (long long)sms * ana_ctas_per_sm(nv, ls) * warps;
     const long long items = (long long)nch * nmembers * ls;
     const long long rounds = (items + slots - 1) / slots;
-    const double eff = useful / ((double)slots * rounds * ((nblk + ls - 1) / ls));
+    const double eff = useful / ((double)slots * rounds * ((nblk + ls - 1) / ls + item_cost));
     if (eff > best_eff + 1e-9) { best_eff = eff; best = ls; }
   }
   return best;
