@@ -759,24 +759,37 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
   }
 
   ANA_STAMP(5);
-  // epilogue: row k = k0 + p + 2 (8 mt + g); columns (re, im) of vector n*4 + t
+  // epilogue: row k = k0 + p + 2 (8 mt + g), column pair (re, im) of staged
+  // vector n*4 + t.  The scaled values are transposed through the warp's q
+  // tile (free after the k-loop; rows of 33 double2 keep the fragment-order
+  // writes conflict-free) so that each vector's 32 degrees leave as one
+  // coalesced 512-byte store instead of 16-byte pieces two degrees apart.
+  {
+    double2* stg = reinterpret_cast<double2*>(qs);   // [4 NT][33] double2 (4 NT * 33 * 2 <= 32 kQS)
+    static_assert(4 * NT * 33 * 2 <= kChunk * kQS, "staging fits the q tile");
+    __syncwarp();
 #pragma unroll
-  for (int p = 0; p < 2; ++p)
+    for (int p = 0; p < 2; ++p)
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      const int k = k0 + p + 2 * (8 * mt + g);
-      if (k >= nout) continue;
-      const double gs = gsv[p][mt];
+      for (int mt = 0; mt < 2; ++mt) {
+        const int kl = p + 2 * (8 * mt + g);
+        const double gs = gsv[p][mt];
 #pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        // MP = 2: n-tiles [NT/2, NT) are the second member's vectors
-        const int h = (MP == 2 && n >= NT / 2) ? 1 : 0;
-        const int v = (n - h * (NT / 2)) * 4 + t;
-        if (v < a.nv)
-          out[(size_t)h * a.out_mstride + (size_t)v * a.out_vstride + (size_t)r * a.out_rstride + r + k] =
-              make_double2(acc[p][mt][n][0] * gs, acc[p][mt][n][1] * gs);
+        for (int n = 0; n < NT; ++n)
+          stg[(n * 4 + t) * 33 + kl] = make_double2(acc[p][mt][n][0] * gs, acc[p][mt][n][1] * gs);
       }
+    __syncwarp();
+    const bool inrow = k0 + lane < nout;
+#pragma unroll
+    for (int vs = 0; vs < 4 * NT; ++vs) {
+      // MP = 2: staged vectors [2 NT, 4 NT) are the second member's
+      const int h = (MP == 2 && vs >= 2 * NT) ? 1 : 0;
+      const int v = vs - h * 2 * NT;
+      if (v < a.nv && inrow)
+        out[(size_t)h * a.out_mstride + (size_t)v * a.out_vstride + (size_t)r * a.out_rstride + r + k0 + lane] =
+            stg[vs * 33 + lane];
     }
+  }
   ANA_STAMP(6);
 }
 
