@@ -52,7 +52,9 @@ int swsdc_plan_destroy(swsdc_plan* plan);
  * fused shared-memory grid kernel fits (used by the tests to check both paths). */
 int swsdc_plan_config(swsdc_plan* plan, int key, int value);
 /* Pre-size the scratch workspace for up to `fields` simultaneous fields (so no
- * allocation happens later, e.g. during CUDA graph capture). */
+ * allocation happens later, e.g. during CUDA graph capture).  Workspaces a stream
+ * capture has used are pinned: later growth allocates fresh buffers and keeps the
+ * pinned ones alive until swsdc_plan_destroy, so captured graphs stay valid. */
 int swsdc_plan_reserve(swsdc_plan* plan, int fields);
 
 /* TransformPlan.synthesize (spharm.py:258-260); coefficients at truncation
@@ -126,6 +128,11 @@ int swsdc_sweep_node(int truncation, const swsdc_params* params, double beta, in
                      double* f_i, void* stream);
 /* spharm.truncate / spharm.pad (spharm.py:331-349) over `nmat` (R+1)^2 matrices. */
 int swsdc_resize(const double* in, int r_in, double* out, int r_out, long long nmat, void* stream);
+/* spharm.laplacian / spharm.inv_laplacian (spharm.py:313-328) over `nmat` (R+1)^2
+ * matrices: multiply (inverse = 0) or divide (inverse = 1, s = 0 column set to 0) by
+ * -s(s+1)/radius^2; in == out allowed.  1 (usage) if radius <= 0. */
+int swsdc_laplacian(const double* in, double* out, int truncation, long long nmat, double radius,
+                    int inverse, void* stream);
 
 /* Upload of `nmat` dense (R+1)^2 spectral matrices from page-locked host memory
  * (cudaHostAlloc / cudaHostRegister) to device `out`: only the s >= r triangle the

@@ -54,6 +54,7 @@ _SIGNATURES = {
     "swsdc_solve_implicit": ([_I, ctypes.POINTER(Params), _D, _P, _I, _P, _P], _I),
     "swsdc_combine": ([_I, ctypes.POINTER(_P), ctypes.POINTER(_D), _LL, _P, _P], _I),
     "swsdc_resize": ([_P, _I, _P, _I, _LL, _P], _I),
+    "swsdc_laplacian": ([_P, _P, _I, _LL, _D, _I, _P], _I),
     "swsdc_upload_coeffs": ([_P, _I, _LL, _P, _P], _I),
     "swsdc_spec_combine_multi": ([_I, _P, _P, _P, _P, _I, _LL, _P, _P, _P], _I),
     "swsdc_copy_finite": ([_P, _P, _LL, _P, _P], _I),

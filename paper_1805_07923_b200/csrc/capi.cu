@@ -35,6 +35,11 @@ struct swsdc_plan {
   void* grid_ws = nullptr;      // large-n_lon F_E path: 5 grids per state
   size_t grid_bytes = 0;
   bool force_split = false;     // option 1: use the large-n_lon F_E path even when it fits
+  // a workspace whose address a stream capture has recorded is "pinned": a
+  // later larger request allocates a new buffer and retires the pinned one
+  // (freed with the plan) instead of freeing memory a CUDA graph still uses
+  bool ws_pinned = false, grid_pinned = false;
+  std::vector<void*> retired;
   // m-sharding caches per row filter: balanced row pairs for synthesis and
   // filtered analysis work lists
   struct Shard {
@@ -81,21 +86,42 @@ size_t x_bytes_for(const swsdc_plan* p, int nv, int nmembers) {
   return sizeof(double) * (size_t)make_xlayout(p->dev.R, p->dev.Jh, nv).mstride * nmembers + 256;
 }
 
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+
+// Drop a workspace buffer before reallocation: freed if no captured graph can
+// reference it, else kept alive until the plan is destroyed.
+template <typename T>
+int retire(swsdc_plan* p, T*& buf, size_t& bytes, bool& pinned) {
+  if (buf) {
+    if (pinned) {
+      p->retired.push_back(buf);
+    } else {
+      SW_CUDA(cudaDeviceSynchronize());
+      SW_CUDA(cudaFree(buf));
+    }
+  }
+  buf = nullptr;
+  bytes = 0;
+  pinned = false;
+  return kOk;
+}
+
 int ensure_ws(swsdc_plan* p, int n_eo, size_t x_bytes, int n_y, cudaStream_t st = 0) {
   const size_t need = (size_t)n_eo * field_bytes(p) + x_bytes + (size_t)n_y * y_bytes(p) + 256;
+  if (capturing(st)) {
+    // growing the workspace cannot happen during graph capture
+    if (need > p->ws_bytes) {
+      set_error("workspace too small during stream capture; call swsdc_plan_reserve first");
+      return kUsage;
+    }
+    p->ws_pinned = true;
+    return kOk;
+  }
   if (need <= p->ws_bytes) return kOk;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  // growing the workspace cannot happen during graph capture
-  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
-    set_error("workspace too small during stream capture; call swsdc_plan_reserve first");
-    return kUsage;
-  }
-  if (p->ws) {
-    SW_CUDA(cudaDeviceSynchronize());
-    SW_CUDA(cudaFree(p->ws));
-    p->ws = nullptr;
-    p->ws_bytes = 0;
-  }
+  SW_TRY(retire(p, p->ws, p->ws_bytes, p->ws_pinned));
   SW_CUDA(cudaMalloc(&p->ws, need));
   p->ws_bytes = need;
   return kOk;
@@ -253,15 +279,13 @@ int pick_ana_split(int nch, int nmembers, int nv, int Jh) {
 // capture it cannot grow: returns false so the caller can use the fused kernel.
 int grow_grid_ws(swsdc_plan* p, size_t need, cudaStream_t st, bool* ok) {
   *ok = true;
-  if (need <= p->grid_bytes) return kOk;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
-    *ok = false;
+  if (capturing(st)) {
+    if (need > p->grid_bytes) { *ok = false; return kOk; }
+    p->grid_pinned = true;
     return kOk;
   }
-  if (p->grid_ws) { SW_CUDA(cudaDeviceSynchronize()); SW_CUDA(cudaFree(p->grid_ws)); }
-  p->grid_ws = nullptr;
-  p->grid_bytes = 0;
+  if (need <= p->grid_bytes) return kOk;
+  SW_TRY(retire(p, p->grid_ws, p->grid_bytes, p->grid_pinned));
   SW_CUDA(cudaMalloc(&p->grid_ws, need));
   p->grid_bytes = need;
   return kOk;
@@ -521,6 +545,7 @@ int swsdc_plan_destroy(swsdc_plan* p) {
   for (void* ptr : p->owned) cudaFree(ptr);
   if (p->ws) cudaFree(p->ws);
   if (p->grid_ws) cudaFree(p->grid_ws);
+  for (void* ptr : p->retired) cudaFree(ptr);
   delete p;
   return kOk;
 }
@@ -538,13 +563,8 @@ int swsdc_plan_reserve(swsdc_plan* p, int fields) {
   if (!swe_grid_fits(p->dev) || p->force_split ||
       swe_split_preferred(p->dev, (long long)p->dev.Jh * std::max(1, fields / 5))) {
     const size_t need = sizeof(double2) * (size_t)p->dev.I * (p->dev.Jh + 1) * fields;
-    if (need > p->grid_bytes) {
-      if (p->grid_ws) { SW_CUDA(cudaDeviceSynchronize()); SW_CUDA(cudaFree(p->grid_ws)); }
-      p->grid_ws = nullptr;
-      p->grid_bytes = 0;
-      SW_CUDA(cudaMalloc(&p->grid_ws, need));
-      p->grid_bytes = need;
-    }
+    bool ok = true;
+    SW_TRY(grow_grid_ws(p, need, 0, &ok));
   }
   return ensure_ws(p, 5 * fields, x_bytes_for(p, 7, fields) + x_bytes_for(p, fields, 1),
                    7 * fields);
@@ -882,6 +902,14 @@ int swsdc_resize(const double* in, int r_in, double* out, int r_out, long long n
   if (nmat == 0) return kOk;
   return launch_resize(reinterpret_cast<const double2*>(in), r_in, reinterpret_cast<double2*>(out),
                        r_out, nmat, S(stream));
+}
+
+int swsdc_laplacian(const double* in, double* out, int truncation, long long nmat, double radius,
+                    int inverse, void* stream) {
+  if (!(radius > 0)) { set_error("radius must be positive"); return kUsage; }
+  if (truncation < 0 || nmat < 0) { set_error("bad laplacian arguments"); return kUsage; }
+  return launch_laplacian(reinterpret_cast<const double2*>(in), reinterpret_cast<double2*>(out),
+                          truncation, nmat, radius, inverse != 0, S(stream));
 }
 
 // Staircase cover of the s >= r triangle: block k holds rows [r0, r1) and

@@ -8,6 +8,7 @@
 //   solve_implicit    per-(r, s) 2x2 + scalar closed form (implicit.py:31-49)
 //   combine           sum_k w_k x_k (sdc.py:211-220, PrognosticState algebra swe.py:77-102)
 //   resize            truncate / pad (spharm.py:331-349)
+//   laplacian         laplacian / inv_laplacian (spharm.py:313-328)
 //   sweep_rhs         b = theta0 + sum_j c_j F_j + ... (sdc.py:185-202), fused
 #include <algorithm>
 #include <cstdlib>
@@ -167,6 +168,34 @@ __global__ void combine_kernel(CombineArgs a, long long count) {
     if (a.n > 0) acc = a.w[0] * a.x[0][i];
     for (int k = 1; k < a.n; ++k) acc = fma(a.w[k], a.x[k][i], acc);
     a.out[i] = acc;
+  }
+}
+
+__global__ void laplacian_kernel(const double2* in, double2* out, int R, long long nmat,
+                                 double radius, int inverse) {
+  pdl_wait();
+  pdl_trigger();
+  const long long n = nmat * (R + 1) * (R + 1);
+  const double a2 = radius * radius;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(idx % (R + 1));
+    // lambda_s = -s (s + 1) / a^2 with the reference's rounding (spharm.py:307-310):
+    // the product of two small integers is exact, one correctly rounded division
+    const double lam = __ddiv_rn(-(double)s * ((double)s + 1.0), a2);
+    const double2 v = in[idx];
+    double2 o;
+    if (!inverse) {
+      o = make_double2(__dmul_rn(v.x, lam), __dmul_rn(v.y, lam));
+    } else if (s == 0) {
+      o = make_double2(0.0, 0.0);     // the singular s = 0 mode is gauged to zero
+    } else {
+      // numpy divides complex by real as Smith's complex division with a zero
+      // imaginary part: one correctly rounded reciprocal, then two products
+      const double scl = __drcp_rn(lam);
+      o = make_double2(__dmul_rn(v.x, scl), __dmul_rn(v.y, scl));
+    }
+    out[idx] = o;
   }
 }
 
@@ -450,6 +479,17 @@ int launch_sweep_node(int R, const ModelConsts& c, double beta, const SpecCombin
   const dim3 grid((R + 1 + tx - 1) / tx, R + 1, (unsigned)nstates);
   StageScope sc("sweep_node", st);
   SW_CUDA(launch_pdl(sweep_node_kernel, grid, dim3(tx), 0, st, R, c, beta, a, theta, fi, nstates, current_row_filter()));
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_laplacian(const double2* in, double2* out, int R, long long nmat, double radius,
+                     int inverse, cudaStream_t st) {
+  const long long n = nmat * (R + 1) * (R + 1);
+  if (n == 0) return kOk;
+  StageScope sc("laplacian", st);
+  SW_CUDA(launch_pdl(laplacian_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, in, out, R, nmat,
+                     radius, inverse));
   SW_LAUNCH_CHECK();
   return kOk;
 }

@@ -73,5 +73,7 @@ int launch_copy_finite(const double* src, double* dst, long long n, int* bad, cu
 int launch_zero_lower(double2* out, int R, long long nmat, cudaStream_t st);
 int launch_resize(const double2* in, int rin, double2* out, int rout, long long nmat,
                   cudaStream_t st);
+int launch_laplacian(const double2* in, double2* out, int R, long long nmat, double radius,
+                     int inverse, cudaStream_t st);
 
 }  // namespace swsdc

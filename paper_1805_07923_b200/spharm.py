@@ -403,28 +403,29 @@ def laplacian_eigenvalues(truncation: int, radius: float) -> np.ndarray:
     return -s * (s + 1.0) / (radius * radius)
 
 
-def _lam_tensor(c: torch.Tensor, radius: float) -> torch.Tensor:
-    return torch.as_tensor(laplacian_eigenvalues(c.shape[-1] - 1, radius), device=c.device)
+def _laplacian(coeffs, radius: float, inverse: int):
+    if radius <= 0:
+        raise ValueError("radius must be positive")
+    c, host = _to_device(coeffs, torch.complex128, _dev_of(coeffs))
+    c = c.contiguous()
+    out = torch.empty_like(c)
+    lib = _lib.load()
+    with _dev_guard(c.device):
+        _lib.check(lib.swsdc_laplacian(_ptr(c), _ptr(out), c.shape[-1] - 1,
+                                       math.prod(c.shape[:-2]), float(radius), inverse,
+                                       _stream_ptr(c.device)))
+    return _out(out, host)
 
 
 def laplacian(coeffs, radius: float):
-    """Multiply by -s(s+1)/a^2 (spharm.py:313-317)."""
-    if radius <= 0:
-        raise ValueError("radius must be positive")
-    c, host = _to_device(coeffs, torch.complex128, _dev_of(coeffs))
-    return _out(c * _lam_tensor(c, radius), host)
+    """Multiply by -s(s+1)/a^2 (spharm.py:313-317); one library kernel."""
+    return _laplacian(coeffs, radius, 0)
 
 
 def inv_laplacian(coeffs, radius: float):
-    """Inverse Laplacian with the s = 0 column gauged to zero (spharm.py:320-328)."""
-    if radius <= 0:
-        raise ValueError("radius must be positive")
-    c, host = _to_device(coeffs, torch.complex128, _dev_of(coeffs))
-    lam = _lam_tensor(c, radius)
-    lam[0] = 1.0
-    out = c / lam
-    out[..., 0] = 0.0
-    return _out(out, host)
+    """Inverse Laplacian with the s = 0 column gauged to zero (spharm.py:320-328),
+    rounded as numpy's complex-by-real division; one library kernel."""
+    return _laplacian(coeffs, radius, 1)
 
 
 def _dev_of(x):

@@ -73,3 +73,28 @@ def test_instability_is_reported_with_step_index():
     with pytest.raises(stepper.InstabilityError) as ei:
         st.run(50)
     assert 0 <= ei.value.step < 50   # 0-based, as the reference loop index
+
+
+def test_eager_growth_after_capture_keeps_the_graph_valid():
+    """A captured step bakes the plan workspaces into its graph; an eager call
+    on the same plan that needs more scratch (a bigger batch) must not free
+    them (capi.cu ensure_ws / grow_grid_ws retire pinned buffers)."""
+    from paper_1805_07923_b200 import mlsdc, stepper, swe, workloads
+    params, oparams = earth()
+    hier = mlsdc.build_hierarchy(params, 31, 3, 15, 2, grid_fine=(96, 48), grid_coarse=(48, 24))
+    x = workloads.seeded_state(31, 6)
+    st = stepper.MLSDCStepper(hier, 600.0, 2, swe.PrognosticState(torch.as_tensor(x).cuda()))
+    st.run(1)
+    # eager F_E and analyses on a much larger batch through the same plans
+    big = torch.as_tensor(np.stack([workloads.seeded_state(31, k) for k in range(40)])).cuda()
+    hier.fine.rhs.eval_f_e(swe.PrognosticState(big))
+    grids = hier.fine.plan.synthesize(big.reshape(-1, 32, 32))
+    hier.fine.plan.analyze(grids)
+    torch.cuda.synchronize()
+    st.set_state(swe.PrognosticState(torch.as_tensor(x).cuda()))
+    y = st.run(1).numpy()
+    oh = orc.OracleHierarchy(orc.OracleLevel(31, 3, oparams, (96, 48)),
+                             orc.OracleLevel(15, 2, oparams, (48, 24)))
+    want = orc.mlsdc_step(x, 600.0, 2, oh)
+    for f in range(3):
+        assert rel_err(y[f], want[f]) < 1e-9
