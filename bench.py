@@ -42,6 +42,11 @@ FP64_FALLBACK_TFLOPS = 36.9   # profiles/fp64_peak_r01.txt (tools/fp64_peak.cu o
 # ----------------------------------------------------------------------------
 # algorithmic work per field
 # ----------------------------------------------------------------------------
+def config_dict():
+    """The workload, identical in both arms (--impl ours / reference)."""
+    return {"workload": WORKLOAD, "R": R, "grid": [I, J], "fields": NF}
+
+
 def legendre_flops(Rr, Jj):
     T = (Rr + 1) * (Rr + 2) // 2
     return 2.0 * T * Jj                        # per field per direction
@@ -143,21 +148,23 @@ class ClockSampler:
 # CPU baseline: the oracle port (numpy, reference dense-table algorithm)
 # ----------------------------------------------------------------------------
 _PLAN = None
+_BATCH = None
 
 
 def _cpu_init():
-    """Pool initializer: one dense-table oracle plan per worker (plan build is
-    setup, excluded from timing as in the reference harness, harness.py:234)."""
-    global _PLAN
+    """Pool initializer: one dense-table oracle plan per worker and the seeded
+    input batch (plan build and input generation are setup, excluded from
+    timing as in the reference harness, harness.py:234)."""
+    global _PLAN, _BATCH
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import swsdc_oracle as orc
+    from paper_1805_07923_b200 import workloads
     _PLAN = orc.OraclePlan(R, I, J)
+    _BATCH = workloads.transform_batch(R, NF)
 
 
 def _cpu_pair(idx):
-    from paper_1805_07923_b200 import workloads
-    c = workloads.spectral_noise(np.random.default_rng(idx), R, workloads.RMS_TARGETS[idx % 3],
-                                 idx % 3 != 0)
+    c = _BATCH[idx % NF]
     t0 = time.perf_counter()
     g = _PLAN.synthesize(c)
     c2 = _PLAN.analyze(g)
@@ -176,7 +183,9 @@ class CpuPool:
         self.pool.map(_cpu_pair, range(n_workers), chunksize=1)   # warm
 
     def step(self, nfields):
-        """Wall time of one batch of `nfields` field pairs over the pool."""
+        """Wall time of one batch of `nfields` field pairs over the pool (inputs
+        already resident in the workers; only task dispatch and the transforms
+        are inside)."""
         t0 = time.perf_counter()
         res = self.pool.map(_cpu_pair, range(nfields), chunksize=1)
         return time.perf_counter() - t0, max(e for _, e in res)
@@ -184,6 +193,44 @@ class CpuPool:
     def close(self):
         self.pool.close()
         self.pool.join()
+
+
+def pcie_probe(torch, dev, nbytes, reps=30):
+    """Measured PCIe bandwidth of this box for `nbytes` contiguous pinned copies
+    (copy engine): H2D alone, D2H alone, and both directions concurrently."""
+    n = nbytes // 8
+    h = torch.ones(n, dtype=torch.float64).pin_memory()
+    h2 = torch.ones(n, dtype=torch.float64).pin_memory()
+    d = torch.ones(n, dtype=torch.float64, device=dev)
+    d2 = torch.ones(n, dtype=torch.float64, device=dev)
+    s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
+    def run(ops):
+        main = torch.cuda.current_stream(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(2):
+            for st, f in ops:
+                with torch.cuda.stream(st):
+                    f()
+        torch.cuda.synchronize(dev)
+        a.record(main)
+        for st, _ in ops:
+            st.wait_stream(main)
+        for _ in range(reps):
+            for st, f in ops:
+                with torch.cuda.stream(st):
+                    f()
+        for st, _ in ops:
+            main.wait_stream(st)
+        b.record(main)
+        torch.cuda.synchronize(dev)
+        return nbytes * reps / (a.elapsed_time(b) * 1e-3) / 1e9
+
+    up = lambda: d.copy_(h, non_blocking=True)      # noqa: E731
+    dn = lambda: h2.copy_(d2, non_blocking=True)    # noqa: E731
+    return {"h2d_gbps": run([(s1, up)]), "d2h_gbps": run([(s1, dn)]),
+            "duplex_gbps_each": run([(s1, up), (s2, dn)]), "bytes": nbytes,
+            "method": "contiguous pinned cudaMemcpyAsync, copy engine"}
 
 
 def host_cores():
@@ -209,7 +256,8 @@ def run_reference(args, world, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(t_steps) / len(t_steps),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded spectra, SURVEY §8d)",
-        "config": {"workload": WORKLOAD, "R": R, "grid": [I, J], "fields": NF},
+        "config": config_dict(),
+        "parallelism": f"{workers} single-threaded CPU workers (rank 0 only)",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
                          "sample": f"each step: {NF} field pairs over {workers} single-threaded "
                                    f"workers (oracle/swsdc_oracle.py: reference dense tables + "
@@ -322,7 +370,7 @@ def run_ours(args, world, rank, local):
     ev_up, ev_syn, ev_ana, ev_dn = ([torch.cuda.Event() for _ in range(NSET)] for _ in range(4))
     used = [False] * NSET
 
-    def issue_e2e(k):
+    def issue_e2e(k, dense=False):
         i = k % NSET
         with torch.cuda.stream(s_in):
             if used[i]:
@@ -339,28 +387,43 @@ def run_ours(args, world, rank, local):
             ev_ana[i].record(s_cmp)
         with torch.cuda.stream(s_out):
             s_out.wait_event(ev_ana[i])
-            spharm.download_coeffs(o_devs[i], o_pins[i], write_lower=False)
+            if dense:
+                spharm.download_coeffs(o_devs[i], f_pins[i], write_lower=True)
+            else:
+                spharm.download_coeffs(o_devs[i], o_pins[i], write_lower=False)
             ev_dn[i].record(s_out)
         used[i] = True
 
-    for k in range(max(args.warmup, NSET)):
-        issue_e2e(k)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e_s.record(main)
-    for st in (s_in, s_cmp, s_out):
-        st.wait_stream(main)
-    for k in range(args.steps):
-        issue_e2e(k)
-    for st in (s_in, s_cmp, s_out):
-        main.wait_stream(st)
-    e_e.record(main)
-    torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(e_s.elapsed_time(e_e), dist, dev)
+    def run_e2e(dense=False):
+        for k in range(max(args.warmup, NSET)):
+            issue_e2e(k, dense)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_s.record(main)
+        for st in (s_in, s_cmp, s_out):
+            st.wait_stream(main)
+        for k in range(args.steps):
+            issue_e2e(k, dense)
+        for st in (s_in, s_cmp, s_out):
+            main.wait_stream(st)
+        e_e.record(main)
+        torch.cuda.synchronize()
+        return max_over_ranks(e_s.elapsed_time(e_e), dist, dev)
+
+    pcie = pcie_probe(torch, dev, int(NF * (R + 1) * (R + 2) // 2 * 16))
+    e2e_ms = run_e2e()
     e2e_value = world * NF * args.steps / (e2e_ms * 1e-3)
     e2e_err = max(float(np.max(np.abs(o.numpy() - c_host)) / np.max(np.abs(c_host))) for o in o_pins)
+    # the same stream with a dense download into result buffers that were never
+    # zeroed (torch.empty pinned memory): every entry, lower triangle included,
+    # comes from the device -- what a caller without reusable zeroed buffers gets
+    f_pins = [torch.empty_like(c_pins[0]).pin_memory() for _ in range(NSET)]
+    for f in f_pins:
+        f.view(torch.float64).fill_(float("nan"))
+    e2e_dense_ms = run_e2e(dense=True)
+    e2e_dense_err = max(float(np.max(np.abs(o.numpy() - c_host)) / np.max(np.abs(c_host))) for o in f_pins)
 
     mlsdc_lines = {}
     if not args.no_mlsdc:
@@ -381,11 +444,14 @@ def run_ours(args, world, rank, local):
         "fourier_to_grid": NF * fft_flops(I, J),
         "grid_to_fourier": NF * fft_flops(I, J),
     }
+    # minimum HBM bytes per launch = the kernel's input + output: spectral
+    # triangle, Fourier rows (R+1) x J complex, grid I x J real
+    fourier_b = 16.0 * (R + 1) * J
     per_launch_bytes = {
-        "fourier_to_grid": NF * grid_bytes(I, J),
-        "grid_to_fourier": NF * grid_bytes(I, J),
-        "legendre_synthesis": NF * coeff_bytes(R),
-        "legendre_analysis": NF * coeff_bytes(R),
+        "fourier_to_grid": NF * (fourier_b + grid_bytes(I, J)),
+        "grid_to_fourier": NF * (grid_bytes(I, J) + fourier_b),
+        "legendre_synthesis": NF * (coeff_bytes(R) + fourier_b),
+        "legendre_analysis": NF * (fourier_b + coeff_bytes(R)),
     }
     stage_ms = {k: v[1] / max(v[0], 1) for k, v in stages.items()}
     dom = max(stages, key=lambda k: stages[k][1])
@@ -398,12 +464,15 @@ def run_ours(args, world, rank, local):
         pass
     # DRAM bytes per launch of the dominant kernel from the committed ncu --set full
     # capture (profiles/r01/traffic.json), for comparison with the algorithmic bytes
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
-            traffic = json.load(f).get(dom)
-    except Exception:
-        pass
+    traffic = step_traffic = traffic_src = None
+    for rnd in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "traffic.json")) as f:
+                tj = json.load(f)
+            traffic, step_traffic, traffic_src = tj.get(dom), tj.get("step_total"), tj.get("source")
+            break
+        except Exception:
+            pass
     if dom.startswith("legendre"):
         achieved = per_launch_flops[dom] / (dom_ms * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
@@ -424,18 +493,29 @@ def run_ours(args, world, rank, local):
         "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded spectra, amplitude (n+1)^-1.5, rms 1e3/1e-5/1e-6; SURVEY §8d)",
-        "config": {"workload": WORKLOAD, "R": R, "grid": [I, J], "fields": NF,
-                   "global_fields": NF * world, "parallelism": f"replicas x{world} (weak)",
-                   "l2": "flushed before every timed step (256 MiB write + read-back, so no dirty lines carry over)"},
+        "config": config_dict(),
+        "global_fields": NF * world, "parallelism": f"replicas x{world} (weak)",
+        "l2": "flushed before every timed step (256 MiB write + read-back, so no dirty lines carry over)",
         "roofline": roof,
         "step_roofline": {"flops": pair_flops, "achieved_tflops": pair_flops / step_s / 1e12,
-                          "frac_fp64": pair_flops / step_s / 1e12 / peak_fp64},
+                          "frac_fp64": pair_flops / step_s / 1e12 / peak_fp64,
+                          "algorithmic_bytes": NF * 2 * (coeff_bytes(R) + grid_bytes(I, J)),
+                          "kernel_io_bytes": sum(per_launch_bytes.values()),
+                          "dram_bytes_ncu": step_traffic, "dram_source": traffic_src},
         "stages_ms_per_launch": stage_ms,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(NF * (R + 1) * (R + 2) // 2 * 16),
                 "d2h_bytes_per_step": int(NF * (R + 1) * (R + 2) // 2 * 16), "ms_per_step": e2e_ms / args.steps,
                 "roundtrip_err": e2e_err,
+                "dense_fresh_download": {
+                    "value": world * NF * args.steps / (e2e_dense_ms * 1e-3), "unit": UNIT,
+                    "ms_per_step": e2e_dense_ms / args.steps,
+                    "d2h_bytes_per_step": int(NF * (R + 1) ** 2 * 16), "roundtrip_err": e2e_dense_err,
+                    "note": "download_coeffs(write_lower=True) into never-zeroed pinned buffers"},
+                "pcie": pcie,
+                "link_frac": (NF * (R + 1) * (R + 2) // 2 * 16) / (e2e_ms / args.steps * 1e-3) / 1e9
+                             / pcie["duplex_gbps_each"] if pcie.get("duplex_gbps_each") else None,
                 "api": "stream of batches: pinned host (R+1)^2 coefficient matrices -> "
                        "spharm.upload_coeffs (s>=r triangle) -> TransformPlan.synthesize/analyze -> "
                        "spharm.download_coeffs(write_lower=False) into zero-initialised pinned result "
@@ -482,12 +562,15 @@ MLSDC_CONFIGS = {
 SHARDED = {"config3"}
 
 
-def mlsdc_flops(cfg):
-    """Algorithmic FP64 work of one step: per F_E evaluation
-    18 Legendre contractions (2 T J) + 12 FFTs (2.5 I log2 I J), times the
-    evaluation counts 1 + N M_f (fine) and 1 + N (M_c + n_cs M_c) (coarse)."""
+def mlsdc_flops(cfg, contractions=18):
+    """FP64 work of one step: per F_E evaluation `contractions`
+    Legendre contractions (2 T J) + 12 FFTs (2.5 I log2 I J), times the
+    evaluation counts 1 + N M_f (fine) and 1 + N (M_c + n_cs M_c) (coarse).
+    18 = the reference's operation count (the survey's nominal work); the
+    fused F_E here does 12 (5 synthesis + 7 analysis vectors, H folded onto P),
+    so `contractions=12` is the FP64 work actually executed."""
     Rf, (If, Jf), Rc, (Ic, Jc), nf, nc, n_it, ncs, _, _, members = cfg
-    ev = lambda R, I, J: 18 * legendre_flops(R, J) + 12 * fft_flops(I, J)
+    ev = lambda R, I, J: contractions * legendre_flops(R, J) + 12 * fft_flops(I, J)
     n_f = 1 + n_it * (nf - 1)
     n_c = 1 + n_it * ((nc - 1) + ncs * (nc - 1))
     return members * (n_f * ev(Rf, If, Jf) + n_c * ev(Rc, Ic, Jc))
@@ -532,6 +615,7 @@ def run_mlsdc(name, cfg, world, rank, dev, dist, flush_l2, peak_fp64):
     total_members = mine * world if members >= world else members
     value = n_it * total_members * steps / (t_ms * 1e-3)
     fl = mlsdc_flops(cfg) * total_members / members
+    fl12 = mlsdc_flops(cfg, 12) * total_members / members
     out = {"metric": "MLSDC-SH fine sweeps/s (fp64)", "value": value, "unit": "fine sweeps/s",
            "ms_per_step": t_ms / steps, "steps": steps, "members": total_members,
            "config": {"R": [Rf, Rc], "grid": [list(gf), list(gc)], "nodes": [nf, nc],
@@ -539,6 +623,9 @@ def run_mlsdc(name, cfg, world, rank, dev, dist, flush_l2, peak_fp64):
                       "parallelism": f"members sharded x{world}" if members > 1 else "1 GPU"},
            "step_fp64_tflops": fl / (t_ms * 1e-3 / steps) / 1e12 / (world if members > 1 else 1),
            "step_frac_fp64_per_gpu": fl / (t_ms * 1e-3 / steps) / 1e12 / peak_fp64 / (world if members > 1 else 1),
+           "step_frac_fp64_per_gpu_executed": fl12 / (t_ms * 1e-3 / steps) / 1e12 / peak_fp64 / (world if members > 1 else 1),
+           "frac_note": "step_frac_fp64_per_gpu counts the reference's 18 contractions per F_E "
+                        "(SURVEY §8d nominal); _executed counts the 12 this implementation runs",
            "gpu_launches_per_step": 0 if launches == 0 else None,
            "graph_replays_per_step": 1, "finite": finite}
     out["gpu_launches_per_step"] = None  # kernels run inside one CUDA-graph replay per step
@@ -581,6 +668,7 @@ def run_sharded(name, cfg, world, rank, dev, dist, flush_l2, peak_fp64):
                        "parallelism": f"m-sharded x{world} (cyclic rows, latitude pairs, NCCL all-to-all)"},
             "step_fp64_tflops": fl / (t_ms * 1e-3 / steps) / 1e12,
             "step_frac_fp64_per_gpu": fl / (t_ms * 1e-3 / steps) / 1e12 / peak_fp64 / world,
+            "step_frac_fp64_per_gpu_executed": mlsdc_flops(cfg, 12) / (t_ms * 1e-3 / steps) / 1e12 / peak_fp64 / world,
             "scaling": "strong", "finite": finite}
 
 
@@ -604,19 +692,21 @@ def cpu_mlsdc_baseline(name):
     import multiprocessing as mp
     if name == "config3":
         return {"value": None, "unit": "fine sweeps/s", "cores": 0, "kind": "port",
-                "sample": "N/A: the reference's dense (R+1,R+1,J) tables need 126 GB at T1279"}
+                "sample": "N/A in the bench: the reference's dense tables need 126 GB at T1279; "
+                          "the streaming oracle (oracle/swsdc_stream.py) takes ~460 s per step "
+                          "on 8 cores (tests/golden/make_golden_large.py), beyond a bounded sample"}
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     cfg = MLSDC_CONFIGS[name]
     n_it, members = cfg[6], cfg[10]
     if members > 1:
+        # one member step per single-threaded worker; each worker times its own
+        # step after building its hierarchy (plan build excluded, as for 1 core)
         w = max(1, min(host_cores(), 16))
         with mp.get_context("spawn").Pool(w) as pool:
-            t0 = time.perf_counter()
-            pool.map(_cpu_mlsdc, [(name, k) for k in range(w)], chunksize=1)
-            wall = time.perf_counter() - t0
-        return {"value": n_it * w / wall, "unit": "fine sweeps/s", "cores": w, "kind": "port",
-                "sample": f"1 step of {w} members, one single-threaded oracle worker each "
-                          f"(wall incl. oracle plan build)"}
+            t = pool.map(_cpu_mlsdc, [(name, k) for k in range(w)], chunksize=1)
+        return {"value": n_it * w / max(t), "unit": "fine sweeps/s", "cores": w, "kind": "port",
+                "sample": f"1 step of {w} members, one single-threaded oracle worker each; "
+                          f"time = the slowest worker's step (plan build excluded)"}
     with mp.get_context("spawn").Pool(1) as pool:
         t = pool.map(_cpu_mlsdc, [(name, 0)])[0]
     return {"value": n_it / t, "unit": "fine sweeps/s", "cores": 1, "kind": "port",
