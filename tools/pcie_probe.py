@@ -55,4 +55,6 @@ timed("upload triangle zero-copy", [(s1, up_tri)], tri)
 timed("download triangle staircase", [(s1, dn_tri)], tri)
 timed("upload tri + download tri concurrent", [(s1, up_tri), (s2, dn_tri)], tri)
 timed("upload tri + d2h half concurrent", [(s1, up_tri), (s2, d2h_half)], tri)
+timed("h2d half contiguous + download tri concurrent", [(s1, h2d_half), (s2, dn_tri)], tri)
+timed("h2d half contiguous + download tri + upload tri", [(s1, h2d_half), (s2, dn_tri)], tri)
 json.dump(res, open(os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", "pcie_probe_%s.json" % os.environ.get("PROBE_TAG", "default")), "w"), indent=1)
