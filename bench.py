@@ -78,6 +78,10 @@ def init_dist(world, backend):
     import torch.distributed as dist
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend == "nccl":
+            # communicator init lines (ranks, NVLink/NVLS transport) in the log
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group(backend=backend)
     return dist if world > 1 else None
 
@@ -649,17 +653,22 @@ def run_sharded(name, cfg, world, rank, dev, dist, flush_l2, peak_fp64):
     dist.barrier()
     t_ms = 0.0
     st = st0
-    for _ in range(steps):
+    flags = torch.zeros(steps, dtype=torch.int32, device=dev)
+    for k in range(steps):
         flush_l2()
         a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         st = D.sharded_mlsdc_timestep(st, dt, n_it, hier, spec, ncs)
+        # the reference's per-step finiteness check (harness.py:257-258): a device
+        # flag over this rank's rows, max-reduced over ranks after the loop
+        flags[k] = D.owned_nonfinite(spec, st.data)
         b_.record()
         torch.cuda.synchronize()
         t_ms += a.elapsed_time(b_)
     t_ms = max_over_ranks(t_ms, dist, dev)
+    flags = ex.all_reduce_max(flags)
     full = D.gather_state(ex, spec, st.data)
-    finite = bool(torch.isfinite(torch.view_as_real(full)).all())
+    finite = int(flags.max()) == 0 and bool(torch.isfinite(torch.view_as_real(full)).all())
     fl = mlsdc_flops(cfg)
     return {"metric": "MLSDC-SH fine sweeps/s (fp64)", "value": n_it * steps / (t_ms * 1e-3),
             "unit": "fine sweeps/s", "ms_per_step": t_ms / steps, "steps": steps, "members": 1,

@@ -570,9 +570,21 @@ int swsdc_plan_reserve(swsdc_plan* p, int fields) {
                    7 * fields);
 }
 
+// The public whole-field transforms read every row of their inputs and write every
+// row of their outputs, so they refuse an active m-sharding row filter instead of
+// silently leaving unowned rows unwritten (the sharded pipeline uses swsdc_fe_*).
+static int reject_row_filter(const char* what) {
+  if (current_row_filter().mod > 1) {
+    set_error(std::string(what) + " under an m-sharding row filter: use the staged swsdc_fe_* calls");
+    return kUsage;
+  }
+  return kOk;
+}
+
 int swsdc_synthesize(swsdc_plan* p, const double* coeffs, int r_in, int batch, double* grid,
                      void* stream) {
   if (!p) { set_error("plan is NULL"); return kUsage; }
+  SW_TRY(reject_row_filter("synthesize"));
   if (r_in > p->dev.R) {
     set_error("coefficients at truncation " + std::to_string(r_in) +
               " exceed plan truncation " + std::to_string(p->dev.R));
@@ -589,6 +601,7 @@ int swsdc_synthesize(swsdc_plan* p, const double* coeffs, int r_in, int batch, d
 
 int swsdc_analyze(swsdc_plan* p, const double* grid, int batch, double* coeffs, void* stream) {
   if (!p) { set_error("plan is NULL"); return kUsage; }
+  SW_TRY(reject_row_filter("analyze"));
   if (batch < 0) { set_error("bad batch"); return kUsage; }
   if (batch == 0) return kOk;
   SW_TRY(ensure_ws(p, 0, x_bytes_for(p, batch, 1), 0, S(stream)));
@@ -605,6 +618,7 @@ int swsdc_analyze(swsdc_plan* p, const double* grid, int batch, double* coeffs, 
 int swsdc_synthesize_uv(swsdc_plan* p, const double* psi, const double* chi, int r_in, int batch,
                         double* u, double* v, void* stream) {
   if (!p) { set_error("plan is NULL"); return kUsage; }
+  SW_TRY(reject_row_filter("synthesize_uv"));
   if (r_in > p->dev.R) {
     set_error("coefficients exceed plan truncation");
     return kUsage;
@@ -634,6 +648,7 @@ int swsdc_synthesize_uv(swsdc_plan* p, const double* psi, const double* chi, int
 int swsdc_analyze_divcurl(swsdc_plan* p, const double* u, const double* v, int batch, double* div,
                           double* curl, void* stream) {
   if (!p) { set_error("plan is NULL"); return kUsage; }
+  SW_TRY(reject_row_filter("analyze_divcurl"));
   if (batch < 0) { set_error("bad batch"); return kUsage; }
   if (batch == 0) return kOk;
   const size_t xb = x_bytes_for(p, 4, batch);
@@ -655,10 +670,7 @@ int swsdc_eval_fe(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, c
   SW_TRY(check_params(q));
   if (batch < 0) { set_error("bad batch"); return kUsage; }
   if (batch == 0) return kOk;
-  if (current_row_filter().mod > 1) {
-    set_error("eval_fe under an m-sharding row filter: use the staged swsdc_fe_* calls");
-    return kUsage;
-  }
+  SW_TRY(reject_row_filter("eval_fe"));
   const bool nl = include_nonlinear != 0;
   const int nv = nl ? 7 : 2;
   const size_t xb = x_bytes_for(p, nv, batch);
@@ -841,8 +853,8 @@ int swsdc_copy_finite(const double* src, double* dst, long long n, int* bad, voi
 int swsdc_spec_combine_multi(int nout, const int* nterms, const double* const* x, const double* w,
                              const int* r_in, int r_out, long long nmat, double* const* outs,
                              const int* ext, void* stream) {
-  if (nout < 0 || nout > kMultiOut || nmat < 0 || nmat > 65535 || r_out < 0) {
-    set_error("spec_combine_multi takes 0..16 outputs and <= 65535 matrices");
+  if (nout < 0 || nout > kMultiOut || nmat < 0 || r_out < 0) {
+    set_error("spec_combine_multi takes 0..16 outputs");
     return kUsage;
   }
   MultiCombineArgs a{};
@@ -866,7 +878,7 @@ int swsdc_spec_combine_multi(int nout, const int* nterms, const double* const* x
     a.ext[o] = (ext && ext[o] >= 0 && ext[o] < r_out) ? ext[o] : r_out;
   }
   if (nmat == 0 || nout == 0) return kOk;
-  return launch_spec_combine_multi(a, (int)nmat, S(stream));
+  return launch_spec_combine_multi(a, nmat, S(stream));
 }
 
 int swsdc_sweep_node(int R, const swsdc_params* q, double beta, int n, const double* const* x,

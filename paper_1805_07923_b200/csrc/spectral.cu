@@ -437,19 +437,25 @@ int launch_combine(const CombineArgs& a, long long count, cudaStream_t st) {
   return kOk;
 }
 
-int launch_spec_combine_multi(const MultiCombineArgs& a, int nmat, cudaStream_t st) {
+int launch_spec_combine_multi(const MultiCombineArgs& a, long long nmat, cudaStream_t st) {
   if (a.nout <= 0 || nmat <= 0) return kOk;
   const int row = a.rout + 1;
   const int threads = row >= 256 ? 256 : ((row + 31) / 32) * 32;
-  const long long z = (long long)a.nout * nmat;
-  if (z > 65535) {
-    set_error("spec_combine_multi: outputs x matrices exceed one launch");
-    return kUsage;
-  }
+  // gridDim.z = nout x matrices <= 65535: larger batches go in matrix chunks,
+  // each launch with its inputs / outputs advanced to the chunk's first matrix
+  const long long per = std::max(1LL, 65535LL / a.nout);
   StageScope sc("spec_combine", st);
-  SW_CUDA(launch_pdl(spec_combine_multi_kernel, dim3((row + threads - 1) / threads, row, (unsigned)z),
-                     dim3(threads), 0, st, a, nmat, current_row_filter()));
-  SW_LAUNCH_CHECK();
+  for (long long m0 = 0; m0 < nmat; m0 += per) {
+    const int nm = (int)std::min(per, nmat - m0);
+    MultiCombineArgs c = a;
+    for (int k = 0; k < a.off[a.nout]; ++k)
+      c.x[k] = a.x[k] + (size_t)m0 * (a.rin[k] + 1) * (a.rin[k] + 1);
+    for (int o = 0; o < a.nout; ++o) c.out[o] = a.out[o] + (size_t)m0 * row * row;
+    SW_CUDA(launch_pdl(spec_combine_multi_kernel,
+                       dim3((row + threads - 1) / threads, row, (unsigned)(a.nout * nm)),
+                       dim3(threads), 0, st, c, nm, current_row_filter()));
+    SW_LAUNCH_CHECK();
+  }
   return kOk;
 }
 
@@ -463,7 +469,7 @@ int launch_spec_combine(const SpecCombineArgs& a, long long nmat, cudaStream_t s
     m.ext[0] = a.rout;
     m.nout = 1;
     m.rout = a.rout;
-    return launch_spec_combine_multi(m, (int)nmat, st);
+    return launch_spec_combine_multi(m, nmat, st);
   }
   const long long n = nmat * (a.rout + 1) * (a.rout + 1);
   StageScope sc("spec_combine", st);

@@ -60,7 +60,7 @@ struct MultiCombineArgs {
   int nout;
   int rout;
 };
-int launch_spec_combine_multi(const MultiCombineArgs& a, int nmat, cudaStream_t st);
+int launch_spec_combine_multi(const MultiCombineArgs& a, long long nmat, cudaStream_t st);
 // One sweep node (sdc.py:196-206 fused): b = sum_k w_k x_k (all at R);
 // theta = solve(b, beta); fi = L_G(theta).  nstates = states per input.
 int launch_sweep_node(int R, const ModelConsts& c, double beta, const SpecCombineArgs& a,

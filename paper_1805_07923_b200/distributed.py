@@ -65,9 +65,10 @@ class ShardSpec:
 
 
 class TorchExchanger:
-    """all-to-all over torch.distributed: NCCL all_to_all between GPUs (one
-    collective over NVLink/NVSwitch); on backends without all_to_all (gloo,
-    the CPU tests) paired isend/irecv."""
+    """Collectives over torch.distributed: NCCL all_to_all / all_gather /
+    all_reduce between GPUs (over NVLink/NVSwitch); on gloo (the CPU tests,
+    and several processes sharing one GPU in the GPU tests) paired
+    isend/irecv, with device tensors staged through host memory."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -77,21 +78,43 @@ class TorchExchanger:
         self.native = dist.get_backend(group) == "nccl"
 
     def all_to_all(self, sends: list[torch.Tensor], recv_shapes: list[tuple]) -> list[torch.Tensor]:
-        recvs = [torch.empty(s, dtype=sends[0].dtype, device=sends[0].device) for s in recv_shapes]
-        sends = [t.contiguous() for t in sends]
+        dev = sends[0].device
         if self.native:
-            self.dist.all_to_all(recvs, sends, group=self.group)
+            recvs = [torch.empty(s, dtype=sends[0].dtype, device=dev) for s in recv_shapes]
+            self.dist.all_to_all(recvs, [t.contiguous() for t in sends], group=self.group)
             return recvs
+        host = [t.detach().to("cpu").contiguous() for t in sends]
+        recvs = [torch.empty(s, dtype=sends[0].dtype) for s in recv_shapes]
         reqs = []
         for q in range(self.P):
             if q == self.rank:
-                recvs[q].copy_(sends[q])
+                recvs[q].copy_(host[q])
             else:
-                reqs.append(self.dist.isend(sends[q], q, group=self.group))
+                reqs.append(self.dist.isend(host[q], q, group=self.group))
                 reqs.append(self.dist.irecv(recvs[q], q, group=self.group))
         for r in reqs:
             r.wait()
-        return recvs
+        return [t.to(dev) for t in recvs]
+
+    def all_gather(self, mine: torch.Tensor) -> list[torch.Tensor]:
+        """Every rank's `mine` (equal shapes), in rank order."""
+        if self.native:
+            out = [torch.empty_like(mine) for _ in range(self.P)]
+            self.dist.all_gather(out, mine.contiguous(), group=self.group)
+            return out
+        out = [torch.empty(mine.shape, dtype=mine.dtype) for _ in range(self.P)]
+        self.dist.all_gather(out, mine.detach().to("cpu").contiguous(), group=self.group)
+        return [t.to(mine.device) for t in out]
+
+    def all_reduce_max(self, t: torch.Tensor) -> torch.Tensor:
+        """Elementwise max over ranks (in place on NCCL; returns the result)."""
+        import torch.distributed as dist
+        if self.native:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+            return t
+        h = t.detach().to("cpu")
+        dist.all_reduce(h, op=dist.ReduceOp.MAX, group=self.group)
+        return h.to(t.device)
 
 
 class LocalExchanger:
@@ -111,6 +134,13 @@ class LocalExchanger:
 class _LocalRank:
     def __init__(self, hub: LocalExchanger, rank: int):
         self.hub, self.P, self.rank = hub, hub.P, rank
+
+    def all_gather(self, mine):
+        return self.all_to_all([mine] * self.P, [tuple(mine.shape)] * self.P)
+
+    def all_reduce_max(self, t):
+        got = self.all_to_all([t] * self.P, [tuple(t.shape)] * self.P)
+        return torch.stack(got).amax(dim=0)
 
     def all_to_all(self, sends, recv_shapes):
         hub = self.hub
@@ -172,16 +202,27 @@ def exchange_x(ex, spec: ShardSpec, x: torch.Tensor, R: int, jh4: int) -> torch.
 
 
 def gather_state(ex, spec: ShardSpec, data: torch.Tensor) -> torch.Tensor:
-    """Assemble the full (…, 3, R+1, R+1) state from every rank's own rows."""
+    """Assemble the full (…, 3, R+1, R+1) state from every rank's own rows: one
+    all-gather of each rank's rows, padded to the largest rank's row count."""
     R = data.shape[-1] - 1
-    mine = data[..., spec.rows(R), :].contiguous()
-    sends = [mine] * spec.P
-    shapes = [tuple(data.shape[:-2]) + (len(range(q, R + 1, spec.P)), R + 1) for q in range(spec.P)]
-    recvs = ex.all_to_all(sends, shapes)
+    nmax = len(range(0, R + 1, spec.P))
+    mine = torch.zeros(tuple(data.shape[:-2]) + (nmax, R + 1), dtype=data.dtype,
+                       device=data.device)
+    own = data[..., spec.rows(R), :]
+    mine[..., : own.shape[-2], :] = own
+    got = ex.all_gather(mine)
     out = torch.empty_like(data)
     for q in range(spec.P):
-        out[..., q:R + 1:spec.P, :] = recvs[q]
+        n = len(range(q, R + 1, spec.P))
+        out[..., q:R + 1:spec.P, :] = got[q][..., :n, :]
     return out
+
+
+def owned_nonfinite(spec: ShardSpec, data: torch.Tensor) -> torch.Tensor:
+    """Device int32 flag: 1 if any owned row of `data` holds a non-finite value."""
+    R = data.shape[-1] - 1
+    own = torch.view_as_real(data[..., spec.rows(R), :])
+    return (~torch.isfinite(own)).any().to(torch.int32)
 
 
 # ----------------------------------------------------------------------------
@@ -255,3 +296,26 @@ def sharded_mlsdc_timestep(theta: PrognosticState, dt: float, n_iterations: int,
     from . import mlsdc
     with row_filter(spec.P, spec.rank):
         return mlsdc.mlsdc_timestep(theta, dt, n_iterations, hier, n_coarse_sweeps)
+
+
+def sharded_mlsdc_run(theta: PrognosticState, dt: float, n_iterations: int, hier,
+                      spec: ShardSpec, n_steps: int, n_coarse_sweeps: int = 1,
+                      flags: torch.Tensor | None = None) -> PrognosticState:
+    """n_steps sharded steps with the reference's per-step finiteness contract
+    (harness.py:257-258): after each step a device flag records whether any
+    owned row went non-finite (no host sync inside the loop); the flags are
+    max-reduced over ranks once at the end and the first bad step raises
+    InstabilityError(step) on every rank."""
+    from .stepper import InstabilityError
+    dev = theta.data.device
+    if flags is None:
+        flags = torch.zeros(n_steps, dtype=torch.int32, device=dev)
+    st = theta
+    for k in range(n_steps):
+        st = sharded_mlsdc_timestep(st, dt, n_iterations, hier, spec, n_coarse_sweeps)
+        flags[k] = owned_nonfinite(spec, st.data)
+    flags = hier.fine.rhs.ex.all_reduce_max(flags)
+    bad = torch.nonzero(flags)
+    if bad.numel():
+        raise InstabilityError(int(bad[0]))
+    return st

@@ -58,6 +58,15 @@ def _worker(rank, world, port, R, Jh, fails):
         mine[..., rank:R + 1:world, :] = st[..., rank:R + 1:world, :]
         got = gather_state(ex, spec, mine)
         assert torch.equal(got, st), "gather_state"
+        # --- per-step finiteness flag: a NaN in one rank's own rows reaches every rank
+        from paper_1805_07923_b200.distributed import owned_nonfinite
+        clean = owned_nonfinite(spec, st)
+        assert int(ex.all_reduce_max(clean.view(1))[0]) == 0, "finite flag"
+        dirty = st.clone()
+        dirty[0, 0, 1, 2] = complex(float("nan"), 0.0)   # row 1 belongs to rank 1 % world
+        flag = owned_nonfinite(spec, dirty)
+        assert int(flag) == (1 if rank == 1 % world else 0), "own-row flag"
+        assert int(ex.all_reduce_max(flag.view(1))[0]) == 1, "flag all-reduce"
         # --- ownership covers every row / latitude exactly once
         rows = sorted(r for q in range(world) for r in range(R + 1)[ShardSpec(world, q).rows(R)])
         assert rows == list(range(R + 1))

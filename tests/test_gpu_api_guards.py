@@ -1,0 +1,43 @@
+"""C-ABI guards flagged by the round-1 advisor:
+* spec_combine_multi splits launches whose outputs x matrices exceed the
+  65535 gridDim.z limit (large ensembles) instead of failing;
+* the public whole-field transforms refuse an active m-sharding row filter
+  (they would leave unowned rows unwritten) -- the sharded pipeline uses the
+  staged swsdc_fe_* calls."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def test_spec_combine_multi_beyond_one_launch():
+    from paper_1805_07923_b200 import swe
+    R, members = 7, 1500                      # 16 outputs x 4500 matrices > 65535
+    g = torch.Generator(device="cuda").manual_seed(3)
+    xs = [torch.randn((members, 3, R + 1, R + 1), dtype=torch.complex128, device="cuda",
+                      generator=g).triu_() for _ in range(4)]
+    jobs = [([1.0 + k, -0.5, 0.25 * k], [xs[k % 4], xs[(k + 1) % 4], xs[(k + 2) % 4]], None)
+            for k in range(16)]
+    outs = swe.spec_combine_multi(jobs, R)
+    for (w, x, _), o in zip(jobs, outs):
+        want = sum(wi * xi for wi, xi in zip(w, x))
+        assert torch.allclose(o, want, rtol=0, atol=1e-13)
+
+
+def test_public_transforms_refuse_row_filter():
+    from paper_1805_07923_b200 import distributed, spharm, swe, workloads
+    plan = spharm.TransformPlan(spharm.build_gaussian_grid(24, 48), 15)
+    c = torch.as_tensor(workloads.seeded_state(15, 1)).cuda()
+    g = plan.synthesize(c[0])
+    rhs = swe.ShallowWaterRHS(plan, swe.ModelParams(**workloads.EARTH))
+    with distributed.row_filter(2, 1):
+        for call in (lambda: plan.synthesize(c[0]), lambda: plan.analyze(g),
+                     lambda: plan.synthesize_pair_cos_gradient(c[1], c[2]),
+                     lambda: plan.analyze_vector_div_curl(g, g),
+                     lambda: rhs.eval_f_e(swe.PrognosticState(c))):
+            with pytest.raises(ValueError, match="row filter"):
+                call()
+    # outside the filter the same calls work
+    assert np.isfinite(plan.analyze(g).cpu().numpy()).all()
