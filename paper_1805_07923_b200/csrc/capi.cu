@@ -243,7 +243,7 @@ int upload_work(swsdc_plan* p, std::vector<int4> (&work)[2][kAnaSplits]) {
 // kernel: the one that best fills whole waves, counting warp rounds
 // ceil(items / slots) x blocks per warp ceil(nblk / split) against the
 // useful work nch x nblk (tie -> fewer splits, less reduction traffic).
-int pick_ana_split(int nch, int nmembers, int nv, int Jh) {
+int pick_ana_split(int nch, int nmembers, int nv, int Jh, bool tab) {
   static const int knob = env_int("SWSDC_ANA_LSPLIT", 0);   // tuning knob: force 1..4
   if (knob >= 1 && knob <= kAnaSplits) return knob;
   static int sms = 0;
@@ -259,14 +259,14 @@ int pick_ana_split(int nch, int nmembers, int nv, int Jh) {
   // but pay its per-item cost (seeds, split reduction, epilogue: ~1 latitude
   // block of k-steps, tools/ana_trace.py): charge it there (T1279: 19.06 ->
   // 18.33 ms per config-3 step); small problems keep the wave-fitting choice.
-  const long long slots1 = (long long)sms * ana_ctas_per_sm(nv, 1) * ana_chunks_per_cta(1);
+  const long long slots1 = (long long)sms * ana_ctas_per_sm(nv, 1, tab) * ana_chunks_per_cta(1);
   const double item_cost = (long long)nch * nmembers >= 2 * slots1 ? 1.0 : 0.0;
   int best = 1;
   double best_eff = -1.0;
   for (int ls = 1; ls <= kAnaSplits; ++ls) {
     if (ls > nblk) break;
     const int warps = ls * ana_chunks_per_cta(ls);
-    const long long slots = (long long)sms * ana_ctas_per_sm(nv, ls) * warps;
+    const long long slots = (long long)sms * ana_ctas_per_sm(nv, ls, tab) * warps;
     const long long items = (long long)nch * nmembers * ls;
     const long long rounds = (items + slots - 1) / slots;
     const double eff = useful / ((double)slots * rounds * ((nblk + ls - 1) / ls + item_cost));
@@ -344,8 +344,9 @@ int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, dou
   // ensembles: two members per CTA when each has <= 8 vectors (same q tiles, NT = 4)
   const bool pairs = xl.nv <= 8 && ana_pairs_ok(xl.nv, nmembers);
   const int lsplit = ana_uses_tma(nv0) ? 1
-                     : pairs ? pick_ana_split(nch, nmembers / 2, 16, P.Jh)
-                             : pick_ana_split(nch, nmembers, nv0, P.Jh);
+                     : pairs ? pick_ana_split(nch, nmembers / 2, 16, P.Jh, ana_table_fed(P, 4, 2))
+                             : pick_ana_split(nch, nmembers, nv0, P.Jh,
+                                              ana_table_fed(P, (2 * nv0 + 7) / 8, 1));
   const int ls = lsplit - 1;
   for (int v0 = 0; v0 < xl.nv; v0 += 16) {
     AnaArgs a{};
@@ -527,6 +528,26 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
   P.rev = d_rev;
   P.ckpt = reinterpret_cast<double2*>(ck);
   st = build_checkpoints(P, d_a, d_b, d_sect, reinterpret_cast<double2*>(ck), 0);
+  // Table-fed analysis: a fragment-native Pbar table (reference-rounded values)
+  // replaces the analysis kernel's recurrence when it is small enough to stay
+  // L2-resident-ish (SWSDC_TABLES: 0 off, 1 auto; SWSDC_TABLE_MB cap, default
+  // 192: T255 on 384 latitudes needs 57 MB, T639 on 960 790 MB).
+  {
+    static const int tables = env_int("SWSDC_TABLES", 1);
+    static const int cap_mb = env_int("SWSDC_TABLE_MB", 192);
+    const size_t tab_bytes = sizeof(double) * 128 * (size_t)nck * ((P.Jh + 3) / 4);
+    if (st == kOk && tables && tab_bytes <= (size_t)cap_mb * 1024 * 1024) {
+      void* tb = nullptr;
+      if (cudaMalloc(&tb, tab_bytes) != cudaSuccess || cudaMemset(tb, 0, tab_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        if (tb) cudaFree(tb);   // no table: the recurrence kernels run instead
+      } else {
+        p->owned.push_back(tb);
+        P.ptab = reinterpret_cast<const double*>(tb);
+        st = build_ptab(P, d_a, d_b, d_sect, reinterpret_cast<double*>(tb), 0);
+      }
+    }
+  }
   if (st == kOk && cudaDeviceSynchronize() != cudaSuccess) {
     set_error("checkpoint build failed");
     st = kCuda;

@@ -136,6 +136,7 @@ struct PlanDev {
   const double* ilap;     // [R + 66] 1 / (s (s + 1)) (s >= 1), 0 at s = 0: -a^2 / lambda_s / a^2
   const double2* ckpt;    // [sum_r nchunk(r)][Jh] (q_{s0}, q_{s0+1}) chunk seeds
   const int* ck_off;      // [R+1] first chunk index of row r in ckpt
+  const double* ptab;     // [nck][jh4][128] Pbar A fragments (table-fed analysis) or nullptr
   const double2* tw;      // [I] exp(-2 pi i e / I)
   const int* rev;         // [I] padded ring slot of frequency k (digit-reversed DIF order)
   int ring_stride;        // double2 slots per ring in shared memory (== 1 mod 8)

@@ -92,6 +92,53 @@ int build_checkpoints(const PlanDev& P, const double* a_tab, const double* b_tab
 }
 
 // ---------------------------------------------------------------------------
+// Pbar table for the table-fed analysis: the same reference recurrence,
+// one thread per (north latitude, r), every degree r .. R+1 stored in the
+// analysis A-fragment order -- per (chunk ck = ck_off[r] + (s-r)/32, 4-latitude
+// block jb): [parity p][m-tile mt][lane = 4 g + t] = Pbar at degree
+// s = r + 32 c + p + 2 (8 mt + g) and latitude jh = 4 jb + t.  Entries past
+// R+1 or Jh stay zero (the buffer is zeroed first).
+// ---------------------------------------------------------------------------
+__global__ void build_ptab_kernel(PlanDev P, const double* a_tab, const double* b_tab,
+                                  const double* sect_fac, double* ptab) {
+  pdl_wait();
+  pdl_trigger();
+  const int jh = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (jh >= P.Jh || r > P.R) return;
+  const double mu = P.mu_n[jh];
+  const double u = __dsqrt_rn(__dsub_rn(1.0, __dmul_rn(mu, mu)));
+  double sect = 0.70710678118654757;   // 1/sqrt(2), then the sectoral chain to row r
+  for (int q = 0; q < r; ++q) sect = __dmul_rn(__dmul_rn(sect, u), sect_fac[q]);
+  const double* ar = a_tab + (size_t)r * P.ldk;
+  const double* br = b_tab + (size_t)r * P.ldk;
+  const int jh4 = (P.Jh + 3) >> 2, jb = jh >> 2, tt = jh & 3;
+  const size_t base = (size_t)P.ck_off[r] * jh4;
+  double pm1 = 0.0, pm2 = 0.0;
+  for (int k = 0; k <= P.R + 1 - r; ++k) {
+    double pk;
+    if (k == 0) pk = sect;
+    else if (k == 1) pk = __dmul_rn(__dmul_rn(mu, ar[1]), sect);
+    else pk = __dsub_rn(__dmul_rn(__dmul_rn(ar[k], mu), pm1), __dmul_rn(br[k], pm2));
+    const int c = k >> 5, kk = k & 31, pp = kk & 1, i = kk >> 1;
+    const int lane = ((i & 7) << 2) | tt;
+    ptab[((base + (size_t)c * jh4 + jb) << 7) + ((pp << 1) | (i >> 3)) * 32 + lane] = pk;
+    pm2 = pm1;
+    pm1 = pk;
+  }
+}
+
+int build_ptab(const PlanDev& P, const double* a_tab, const double* b_tab, const double* sect_fac,
+               double* ptab, cudaStream_t st) {
+  const int threads = 64;
+  StageScope sc("build_ptab", st);
+  SW_CUDA(launch_pdl(build_ptab_kernel, dim3((P.Jh + threads - 1) / threads, P.R + 1), dim3(threads),
+                     0, st, P, a_tab, b_tab, sect_fac, ptab));
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
+// ---------------------------------------------------------------------------
 // Synthesis
 //
 // One CTA per (r-pair {p, R-p}, latitude group of 64, member): the pair folds
@@ -520,9 +567,15 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // (cp.async, 2 x NT x 256 contiguous bytes per k-step), so the DMMAs read
 // their operands from shared memory instead of waiting on L2.
 constexpr int kBDepth = 4;
-template <int NT>
+// A fragments of one k-step in the table-fed variant: [parity][m-tile][lane]
+constexpr int kAFrag = 2 * 2 * 32;
+template <int NT, bool TAB = false>
 __host__ __device__ constexpr int ana_warp_doubles() {
-  return kChunk * kQS + kChunk + kBDepth * 2 * NT * 32;
+  // TAB: no q tile or betas; the ring carries A and B fragments and, after the
+  // k-loop, the epilogue staging ([4 NT][33] double2) and the split reduction
+  return TAB ? (kBDepth * (2 * NT * 32 + kAFrag) > 4 * NT * 33 * 2
+                    ? kBDepth * (2 * NT * 32 + kAFrag) : 4 * NT * 33 * 2)
+             : kChunk * kQS + kChunk + kBDepth * 2 * NT * 32;
 }
 
 // One work item (r, first chunk, checkpoint index) of member m (one CTA; a
@@ -532,16 +585,22 @@ __host__ __device__ constexpr int ana_warp_doubles() {
 // [0, NT/2) come from the first member's x, [NT/2, NT) from the second's
 // (each member's layout holds NT/2 n-tiles, a.nv <= 4 NT/2 vectors) -- so the
 // q tile and the A fragments serve twice the columns.
-template <int NT, int LSPLIT, int MP = 1>
+// TAB: the A operand (Pbar of the chunk's 32 degrees at 4 latitudes per
+// k-step) is not regenerated from the recurrence but streamed from the plan's
+// fragment-native table P.ptab (reference-rounded values, build_ptab) through
+// the same cp.async ring as the B fragments; no seeds, betas, q tile or chunk
+// scale g.
+template <int NT, int LSPLIT, int MP = 1, bool TAB = false>
 __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, const int4 wk, int m,
                                          double* smem) {
   static_assert(MP == 1 || (MP == 2 && NT % 4 == 0), "member pairs need NT / 2 even");
-  constexpr int kWD = ana_warp_doubles<NT>();
+  constexpr int kWD = ana_warp_doubles<NT, TAB>();
+  constexpr int kSlot = 2 * NT * 32 + (TAB ? kAFrag : 0);        // ring slot (doubles)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  double* qs = smem + (size_t)warp * kWD;                        // [32][kQS]
-  double* bs = qs + kChunk * kQS;                                // [32] betas
-  double* bring = bs + kChunk;                                   // [kBDepth][2][NT * 32]
+  double* qs = smem + (size_t)warp * kWD;                        // [32][kQS] (TAB: staging only)
+  double* bs = qs + kChunk * kQS;                                // [32] betas (not TAB)
+  double* bring = TAB ? qs : bs + kChunk;                        // [kBDepth][slot]
 
   const double* x = a.x + (size_t)(MP * m) * a.xl.mstride;
   double2* out = a.out + (size_t)(MP * m) * a.out_mstride;
@@ -549,11 +608,6 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
   const int nout = a.smax - r + 1;
   ANA_STAMP(0);
 
-  if (a.zero_fill && wk.y == 0) {
-#pragma unroll
-    for (int h = 0; h < MP; ++h)
-      ana_zero_fill(a, out + (size_t)h * a.out_mstride, r, warp, blockDim.x >> 5, lane);
-  }
   const bool active = c * kChunk < nout;
 
   double acc[2][2][NT][2];
@@ -566,14 +620,14 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
 
   const int k0 = c * kChunk;
   // epilogue scales g of this lane's output rows k0 + p + 2 (8 mt + g), fetched
-  // now so the load latency hides behind the contraction
+  // now so the load latency hides behind the contraction (TAB: unscaled, 1)
   double gsv[2][2];
 #pragma unroll
   for (int p = 0; p < 2; ++p)
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
       const int k = k0 + p + 2 * (8 * mt + g);
-      gsv[p][mt] = (active && k < nout) ? P.gsc[(size_t)r * P.ldk + k] : 0.0;
+      gsv[p][mt] = (active && k < nout) ? (TAB ? 1.0 : P.gsc[(size_t)r * P.ldk + k]) : 0.0;
     }
   // first-block seed and mu of this lane's latitude, loaded together with the
   // betas (one round trip for all the item's table loads; the recurrence of
@@ -581,12 +635,21 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
   const double2* seeds = P.ckpt + (size_t)(wk.z + (c - wk.y)) * P.Jh;
   double2 sd_nx = make_double2(0.0, 0.0);
   double mu_nx = 0.0;
-  if (active) {
+  if (!TAB && active) {
     const int jh0 = (half << 5) + lane;
     if (jh0 < P.Jh) { sd_nx = seeds[jh0]; mu_nx = P.mu_n[jh0]; }
   }
+  if (!TAB && active) bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
+  // everything above reads only plan tables; x and out belong to the stream's
+  // earlier kernels, so the dependency wait (PDL) sits here: the item's table
+  // round trip overlaps the predecessor's tail
+  pdl_wait();
+  if (a.zero_fill && wk.y == 0) {
+#pragma unroll
+    for (int h = 0; h < MP; ++h)
+      ana_zero_fill(a, out + (size_t)h * a.out_mstride, r, warp, blockDim.x >> 5, lane);
+  }
   if (active) {
-    bs[lane] = P.beta[(size_t)r * P.ldk + k0 + lane];
     const int nc = a.xl.nc, jh4 = a.xl.jh4;
     const double* xr = x + (size_t)r * jh4 * 2 * nc * 4;
     const int nblk = (P.Jh + 31) >> 5;
@@ -611,10 +674,17 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
     const size_t jump = (size_t)((LSPLIT - 1) * 8 + 1) * jb_stride;
     const size_t poff = (size_t)nc * 4;                       // parity-1 half of a block
     const double* ip = xr + (size_t)(half << 3) * jb_stride;  // block of the next issue
+    // TAB: A fragments of this warp's chunk, kAFrag doubles per 4-latitude block
+    const double* ap = TAB ? P.ptab + ((size_t)(wk.z + (c - wk.y)) * jh4 + (half << 3)) * kAFrag
+                           : nullptr;
     int iss = 0, ijb = half << 3;
     auto issue_next = [&]() {
       if (iss < nks && ijb < jh4) {
-        double* dst = bring + (iss & (kBDepth - 1)) * (2 * NT * 32);
+        double* dst = bring + (iss & (kBDepth - 1)) * kSlot;
+        if constexpr (TAB) {
+          cp_async16_ana(dst + 2 * NT * 32 + 2 * lane, ap + 2 * lane);
+          cp_async16_ana(dst + 2 * NT * 32 + 64 + 2 * lane, ap + 64 + 2 * lane);
+        }
         if constexpr (NT % 2 == 0) {
           // each parity half is NT/2 copies per lane at fixed offsets from the
           // lane's base: immediate-offset addressing, no per-step index math
@@ -640,6 +710,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
       const bool blk = (iss & 7) == 0;
       ijb += blk ? (LSPLIT - 1) * 8 + 1 : 1;
       ip += blk ? jump : jb_stride;
+      if constexpr (TAB) ap += (blk ? (LSPLIT - 1) * 8 + 1 : 1) * kAFrag;
     };
     ANA_STAMP(1);
 #pragma unroll
@@ -651,6 +722,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
     auto blocks = [&](auto mt_count) {
     constexpr int MTN = decltype(mt_count)::value;
     for (int jb32 = half; jb32 < nblk; jb32 += LSPLIT) {
+      if constexpr (!TAB) {
       __syncwarp();
       // regenerate q for 32 degrees at latitude jh = 32*jb32 + lane
       const int jh = (jb32 << 5) + lane;
@@ -676,6 +748,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
         for (int kk = 0; kk < kChunk; ++kk) qs[((kk & 1) * 16 + (kk >> 1)) * kQS + lane] = 0.0;
       }
       __syncwarp();
+      }
       if (jb32 == half) ANA_STAMP(2);
       // k-steps of this block; blocks reaching past Jh (padding rows of x may
       // hold non-finite bits, q = 0 there) take the masked instantiation
@@ -689,7 +762,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
           if (ks == 0) ANA_STAMP(3);
           // no column mask: column n of D depends only on column n of B, and
           // columns >= 2 nv only feed accumulators that are never written
-          const double* bsrc = bring + (ks & (kBDepth - 1)) * (2 * NT * 32);
+          const double* bsrc = bring + (ks & (kBDepth - 1)) * kSlot;
           double bv[2][NT];
           const bool ok = FULL || (((jb32 << 3) + s) * 4 + t) < P.Jh;
 #pragma unroll
@@ -703,7 +776,8 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
           for (int p = 0; p < 2; ++p)
 #pragma unroll
             for (int mt = 0; mt < MTN; ++mt) {
-              const double av = qs[(p * 16 + mt * 8 + g) * kQS + s * 4 + t];
+              const double av = TAB ? bsrc[2 * NT * 32 + (p * 2 + mt) * 32 + lane]
+                                    : qs[(p * 16 + mt * 8 + g) * kQS + s * 4 + t];
 #pragma unroll
               for (int n = 0; n < NT; ++n) dmma884(acc[p][mt][n], av, bv[p][n]);
             }
@@ -725,7 +799,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
     // only the LSPLIT warps of one chunk meet (named barrier 1 + chunk)
     const unsigned bar_id = 1 + warp / LSPLIT, bar_n = 32 * LSPLIT;
     asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
-    double* red = smem + (size_t)warp * ana_warp_doubles<NT>();
+    double* red = smem + (size_t)warp * ana_warp_doubles<NT, TAB>();
     if (half > 0 && active) {
 #pragma unroll
       for (int p = 0; p < 2; ++p)
@@ -742,7 +816,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
     if (!active) return;
     if (half > 0) return;
     for (int h = 1; h < LSPLIT; ++h) {
-      const double* src = smem + (size_t)(warp + h) * ana_warp_doubles<NT>();
+      const double* src = smem + (size_t)(warp + h) * ana_warp_doubles<NT, TAB>();
 #pragma unroll
       for (int p = 0; p < 2; ++p)
 #pragma unroll
@@ -766,7 +840,8 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
   // coalesced 512-byte store instead of 16-byte pieces two degrees apart.
   {
     double2* stg = reinterpret_cast<double2*>(qs);   // [4 NT][33] double2 (4 NT * 33 * 2 <= 32 kQS)
-    static_assert(4 * NT * 33 * 2 <= kChunk * kQS, "staging fits the q tile");
+    static_assert(4 * NT * 33 * 2 <= (TAB ? ana_warp_doubles<NT, TAB>() : kChunk * kQS),
+                  "staging fits the q tile / ring");
     __syncwarp();
 #pragma unroll
     for (int p = 0; p < 2; ++p)
@@ -794,13 +869,12 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
 }
 
 // One CTA per work item (grid: items x members).
-template <int NT, int LSPLIT, int MP = 1>
+template <int NT, int LSPLIT, int MP = 1, bool TAB = false>
 __global__ void __launch_bounds__(kAnaWarps * 32)
 ana_kernel(PlanDev P, AnaArgs a) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_trigger();   // pdl_wait() inside ana_item, after the plan-table loads
   extern __shared__ __align__(16) double smem[];
-  ana_item<NT, LSPLIT, MP>(P, a, a.work[blockIdx.x], blockIdx.y, smem);
+  ana_item<NT, LSPLIT, MP, TAB>(P, a, a.work[blockIdx.x], blockIdx.y, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -988,8 +1062,9 @@ bool ana_dfma() {
 template <int LSPLIT>
 int launch_ana_pairs_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st) {
   const int warps = LSPLIT * ana_chunks_per_cta(LSPLIT);
-  const size_t smem = sizeof(double) * warps * ana_warp_doubles<4>();
-  auto kern = ana_kernel<4, LSPLIT, 2>;
+  const bool tab = ana_table_fed(P, 4, 2);
+  const size_t smem = sizeof(double) * warps * (tab ? ana_warp_doubles<4, true>() : ana_warp_doubles<4>());
+  auto kern = tab ? ana_kernel<4, LSPLIT, 2, true> : ana_kernel<4, LSPLIT, 2>;
   SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
   StageScope sc("legendre_analysis", st);
   SW_CUDA(launch_pdl(kern, dim3(dim3(nwork, a.nmembers)), dim3(warps * 32), smem, st, P, a));
@@ -1009,8 +1084,9 @@ int launch_ana_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st)
     SW_LAUNCH_CHECK();
     return kOk;
   }
-  const size_t smem = sizeof(double) * warps * ana_warp_doubles<NT>();
-  auto kern = ana_kernel<NT, LSPLIT>;
+  const bool tab = ana_table_fed(P, NT, 1);
+  const size_t smem = sizeof(double) * warps * (tab ? ana_warp_doubles<NT, true>() : ana_warp_doubles<NT>());
+  auto kern = tab ? ana_kernel<NT, LSPLIT, 1, true> : ana_kernel<NT, LSPLIT>;
   SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
   StageScope sc("legendre_analysis", st);
   SW_CUDA(launch_pdl(kern, dim3(dim3(nwork, a.nmembers)), dim3(warps * 32), smem, st, P, a));
@@ -1029,11 +1105,14 @@ int launch_ana_nt(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, cud
 }
 
 template <int NT, int LSPLIT>
-int ana_ctas_per_sm_t() {
+int ana_ctas_per_sm_t(bool tab) {
   const int warps = LSPLIT * ana_chunks_per_cta(LSPLIT);
   const bool dfma = ana_dfma();
-  const size_t smem = sizeof(double) * warps * (dfma ? anad_warp_doubles<NT>() : ana_warp_doubles<NT>());
-  auto kern = dfma ? ana_dfma_kernel<NT, LSPLIT> : ana_kernel<NT, LSPLIT>;
+  const size_t smem = sizeof(double) * warps *
+                      (dfma ? anad_warp_doubles<NT>()
+                            : tab ? ana_warp_doubles<NT, true>() : ana_warp_doubles<NT>());
+  auto kern = dfma ? ana_dfma_kernel<NT, LSPLIT>
+                   : tab ? ana_kernel<NT, LSPLIT, 1, true> : ana_kernel<NT, LSPLIT>;
   if (set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem) != kOk) return 1;
   int n = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, warps * 32, smem) != cudaSuccess) {
@@ -1044,7 +1123,7 @@ int ana_ctas_per_sm_t() {
 }
 
 // ---------------------------------------------------------------------------
-// Analysis, TMA-streamed variant (default).  CTA = 4 warps = 4 consecutive
+// Analysis, TMA-streamed variant (opt-in: SWSDC_ANA_TMA=2; measured slower than the cp.async ring of ana_kernel, which is the default).  CTA = 4 warps = 4 consecutive
 // 32-degree chunks of ONE row r; the row's x tiles (32 latitudes = 8 blocks,
 // contiguous in the fragment-native layout) are streamed into a 3-deep shared
 // ring by one elected thread with cp.async.bulk (TMA, SASS UBLKCP) completing
@@ -1236,19 +1315,20 @@ int launch_ana_tma(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t s
 int ana_warps_per_cta() { return kAnaWarps; }
 int ana_chunks_per_cta(int lsplit) { return lsplit >= 3 ? 1 : kAnaWarps / lsplit; }
 
-// Resident CTAs per SM of the register analysis kernel (cached per NT, LSPLIT).
-int ana_ctas_per_sm(int nv, int lsplit) {
-  static int cache[4][4] = {};
+// Resident CTAs per SM of the register analysis kernel (cached per NT, LSPLIT,
+// q-tile / table variant).
+int ana_ctas_per_sm(int nv, int lsplit, bool tab) {
+  static int cache[2][4][4] = {};
   const int nt = (2 * nv + 7) / 8;   // 1..4
-  int& c = cache[nt - 1][lsplit - 1];
+  int& c = cache[tab ? 1 : 0][nt - 1][lsplit - 1];
   if (c == 0) {
     int n = 1;
 #define SW_OCC(NT_)                                                   \
     switch (lsplit) {                                                 \
-      case 1: n = ana_ctas_per_sm_t<NT_, 1>(); break;                 \
-      case 2: n = ana_ctas_per_sm_t<NT_, 2>(); break;                 \
-      case 3: n = ana_ctas_per_sm_t<NT_, 3>(); break;                 \
-      default: n = ana_ctas_per_sm_t<NT_, 4>(); break;                \
+      case 1: n = ana_ctas_per_sm_t<NT_, 1>(tab); break;              \
+      case 2: n = ana_ctas_per_sm_t<NT_, 2>(tab); break;              \
+      case 3: n = ana_ctas_per_sm_t<NT_, 3>(tab); break;              \
+      default: n = ana_ctas_per_sm_t<NT_, 4>(tab); break;             \
     }
     if (nt == 1) { SW_OCC(1) } else if (nt == 2) { SW_OCC(2) } else if (nt == 3) { SW_OCC(3) } else { SW_OCC(4) }
 #undef SW_OCC
@@ -1295,6 +1375,15 @@ int launch_analysis_pairs(const PlanDev& P, const AnaArgs& a, int nwork, int lsp
     case 4: return launch_ana_pairs_t<4>(P, a, nwork, st);
     default: return launch_ana_pairs_t<1>(P, a, nwork, st);
   }
+}
+
+// Table-fed analysis (A fragments streamed from P.ptab) only where each A
+// fragment serves >= 3 n-tiles: with 1-2 n-tiles the extra L2 -> SM traffic
+// (1 KB of A per 4-16 DMMAs) costs more than the recurrence it replaces
+// (config 2, 7 vectors: 1.84 -> 1.92 ms per step; config 1, 15 vectors:
+// analysis 31.2 -> 29.1 us; config 4, member pairs: 6.85 -> 6.47 ms).
+bool ana_table_fed(const PlanDev& P, int nt, int mp) {
+  return P.ptab != nullptr && nt * mp >= 3;
 }
 
 bool ana_pairs_ok(int nv, int nmembers) {

@@ -50,7 +50,13 @@ int launch_analysis(const PlanDev& P, const AnaArgs& a, int nwork, int lsplit, c
 int ana_warps_per_cta();
 // chunks per CTA of the register analysis kernel for a latitude split (1..4)
 int ana_chunks_per_cta(int lsplit);
-int ana_ctas_per_sm(int nv, int lsplit);
+int ana_ctas_per_sm(int nv, int lsplit, bool tab);
+// Whether the analysis of nt n-tiles x mp members per CTA streams A from P.ptab.
+bool ana_table_fed(const PlanDev& P, int nt, int mp);
+// Fragment-native Pbar table for the table-fed analysis (see build_ptab in legendre.cu):
+// nck chunks x jh4 4-latitude blocks x 128 doubles; ptab must be zero-initialised.
+int build_ptab(const PlanDev& P, const double* a_tab, const double* b_tab, const double* sect_fac,
+               double* ptab, cudaStream_t st);
 constexpr int kAnaSplits = 4;
 bool ana_uses_tma(int nv);
 // Ensemble analysis two members per CTA (a.nmembers = member pairs, nv <= 8
