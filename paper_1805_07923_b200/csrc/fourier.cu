@@ -684,6 +684,186 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused SWE grid stage, 9 register FFTs per latitude pair (default for the
+// nonlinear F_E).  The Coriolis terms of swe.py:262-265,
+//   A1 = -f delta - (2 Omega / a) V,   A2 = f zeta - (2 Omega / a) U,
+// are linear in the fields with coefficients constant along a latitude, so
+// their Fourier coefficients are formed directly from the input spectra
+// (kept in shared memory as cf) instead of by a grid round trip: the delta
+// grid is never synthesised (4 inverse FFTs: U/a, V/a, zeta, phi') and only
+// the 5 true products (phi U, phi V, zeta U, zeta V, KE) are transformed back
+// (5 forward FFTs) -- 9 FFTs instead of 12, 5 rings instead of 7, and every
+// FFT round keeps 4-5 of the CTA's 5 warps busy.  Mathematically identical
+// to the grid round trip (band-limited input, r <= R < n_lon / 2): only the
+// rounding differs.
+// ---------------------------------------------------------------------------
+constexpr int kG5Rings = 5;
+constexpr int kG5Threads = 160;
+
+// Fill rings 0..3 with the packed spectra of fields U, V, zeta, phi' (eo
+// fields 0, 1, 2, 4) and cf[q][r] = (F_n, F_s) of fields U, V, zeta, delta
+// (eo fields 0..3) with Im dropped at r = 0, as the grid round trip would.
+__device__ __forceinline__ void fill_g5(double2* rings, double2* cf, const PlanDev& P,
+                                        const double2* eo, size_t fstride) {
+  const int R = P.R, I = P.I, RS = P.ring_stride, nt = blockDim.x;
+  for (int r = threadIdx.x; r <= R; r += nt) {
+    double2 E[5], O[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const double2* src = eo + q * fstride + (size_t)r * P.Jh * 2;
+      E[q] = src[0];
+      O[q] = src[1];
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      if (q < 4) {
+        double2 Fn = d2(E[q].x + O[q].x, E[q].y + O[q].y);
+        double2 Fs = d2(E[q].x - O[q].x, E[q].y - O[q].y);
+        if (r == 0) { Fn.y = 0.0; Fs.y = 0.0; }
+        cf[2 * (q * (R + 1) + r)] = Fn;
+        cf[2 * (q * (R + 1) + r) + 1] = Fs;
+      }
+      if (q == 3) continue;            // no delta ring
+      const int ring = q == 4 ? 3 : q;
+      double2 zp, zm;
+      pair_spectrum(E[q], O[q], r, zp, zm);
+      double2* rg = rings + (size_t)ring * RS;
+      rg[swfft::pad_idx(r)] = zp;
+      if (r != 0) rg[swfft::pad_idx(I - r)] = zm;
+    }
+  }
+  for (int k = R + 1 + threadIdx.x; k < I - R; k += nt)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rings[(size_t)q * RS + swfft::pad_idx(k)] = d2(0.0, 0.0);
+}
+
+// Analysis vectors at (r, jh) from the 5 forward-transformed product rings
+// (PU, PV, ZU, ZV, KE) and the input spectra cf (U, V, zeta, delta); same
+// vectors and weights as swe_out_one.
+__device__ __forceinline__ void swe_out_g5(const double2* rings, const double2* cf,
+                                           const PlanDev& P, double* xm, const XLayout& xl, int r,
+                                           int jh, double w, double wc, double ia, double fn,
+                                           double c2o, bool eq) {
+  const int RS = P.ring_stride, R1 = P.R + 1;
+  double2 PUn, PUs, PVn, PVs, ZUn, ZUs, ZVn, ZVs, Kn, Ks;
+  get_pair(rings, P, r, PUn, PUs);
+  get_pair(rings + RS, P, r, PVn, PVs);
+  get_pair(rings + 2 * RS, P, r, ZUn, ZUs);
+  get_pair(rings + 3 * RS, P, r, ZVn, ZVs);
+  get_pair(rings + 4 * RS, P, r, Kn, Ks);
+  const double2 Un = cf[2 * r], Us = cf[2 * r + 1];
+  const double2 Vn = cf[2 * (R1 + r)], Vs = cf[2 * (R1 + r) + 1];
+  const double2 Zn = cf[2 * (2 * R1 + r)], Zs = cf[2 * (2 * R1 + r) + 1];
+  const double2 Dn = cf[2 * (3 * R1 + r)], Ds = cf[2 * (3 * R1 + r) + 1];
+  // swe.py:262,265 in Fourier space; f = fn north, -fn south
+  const double2 A1n = d2(-fn * Dn.x - c2o * Vn.x, -fn * Dn.y - c2o * Vn.y);
+  const double2 A1s = d2(fn * Ds.x - c2o * Vs.x, fn * Ds.y - c2o * Vs.y);
+  const double2 A2n = d2(fn * Zn.x - c2o * Un.x, fn * Zn.y - c2o * Un.y);
+  const double2 A2s = d2(-fn * Zs.x - c2o * Us.x, -fn * Zs.y - c2o * Us.y);
+  const double rwa = r * wc * ia, wa = wc * ia;
+  // P-vectors: phi, zeta, delta, ke ; H-vectors: phi, zeta, delta
+  put_x(xm, xl, 0, r, jh, ir_scale(PUn, -rwa), ir_scale(PUs, -rwa), eq);
+  put_x(xm, xl, 1, r, jh, cadd2(cscale(A1n, w), ir_scale(ZUn, -rwa)),
+        cadd2(cscale(A1s, w), ir_scale(ZUs, -rwa)), eq);
+  put_x(xm, xl, 2, r, jh, cadd2(cscale(A2n, w), ir_scale(ZVn, rwa)),
+        cadd2(cscale(A2s, w), ir_scale(ZVs, rwa)), eq);
+  put_x(xm, xl, 3, r, jh, cscale(Kn, w), cscale(Ks, w), eq);
+  put_x(xm, xl, 4, r, jh, cscale(PVn, wa), cscale(PVs, wa), eq);
+  put_x(xm, xl, 5, r, jh, cscale(ZVn, wa), cscale(ZVs, wa), eq);
+  put_x(xm, xl, 6, r, jh, cscale(ZUn, wa), cscale(ZUs, wa), eq);
+}
+
+template <int K>
+__host__ __device__ constexpr int g5_min_blocks() { return K >= 20 ? 2 : K == 16 ? 3 : 4; }
+
+// One latitude pair per CTA of 5 warps; CL as in swe_grid_reg_kernel (4-CTA
+// clusters write whole x sectors over DSMEM).  Shared memory: 5 rings, then cf.
+template <int K, bool CL>
+__global__ void __launch_bounds__(kG5Threads, g5_min_blocks<K>()) swe_grid5_kernel(
+    PlanDev P, const double2* eo, long long eo_mstride, double* x, XLayout xl, double omega,
+    double radius, int jh_begin) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(16) double2 rings[];   // [5][RS], then cf [4][R+1][2]
+  const int jh = jh_begin + blockIdx.x;
+  const int m = blockIdx.y;
+  const int RS = P.ring_stride;
+  double2* cf = rings + (size_t)kG5Rings * RS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t fstride = (size_t)(P.R + 1) * P.Jh * 2;
+  GRID_STAMP(0);
+  fill_g5(rings, cf, P, eo + (size_t)m * eo_mstride + (size_t)jh * 2, fstride);
+  __syncthreads();
+  GRID_STAMP(1);
+  if (warp < 4) {   // U/a, V/a, zeta, phi' to the grid
+    double2 wst[3];
+    swfft::cross_twiddles<K, true>(wst, P.tw, lane);
+    double2* ring = rings + (size_t)warp * RS;
+    double2 v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
+    swfft::ring_fft_to<K, true, K == 24>(v, P.tw, lane, wst, ring);
+  }
+  __syncthreads();
+  GRID_STAMP(2);
+  const double mu = P.mu_n[jh];
+  const double ic2 = 1.0 / (1.0 - mu * mu);   // swe.py:180
+  for (int il = threadIdx.x; il < P.I; il += blockDim.x) {
+    const int p = swfft::pad_idx(il);
+    const double2 U = rings[p], V = rings[RS + p], Z = rings[2 * RS + p], Ph = rings[3 * RS + p];
+    // swe.py:271-273 : Phi U, Phi V, zeta U, zeta V, KE = (U^2 + V^2) / (2 (1 - mu^2))
+    rings[p] = d2(Ph.x * U.x, Ph.y * U.y);
+    rings[RS + p] = d2(Ph.x * V.x, Ph.y * V.y);
+    rings[2 * RS + p] = d2(Z.x * U.x, Z.y * U.y);
+    rings[3 * RS + p] = d2(Z.x * V.x, Z.y * V.y);
+    rings[4 * RS + p] = d2(0.5 * (U.x * U.x + V.x * V.x) * ic2, 0.5 * (U.y * U.y + V.y * V.y) * ic2);
+  }
+  __syncthreads();
+  GRID_STAMP(3);
+  {
+    double2 wst[3];
+    swfft::cross_twiddles<K, false>(wst, P.tw, lane);
+    double2* ring = rings + (size_t)warp * RS;
+    double2 v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
+    swfft::ring_fft_to<K, false, K == 24>(v, P.tw, lane, wst, ring);
+  }
+  __syncthreads();
+  GRID_STAMP(4);
+  const double c2o = 2.0 * omega / radius;    // swe.py:179
+  const double ia = 1.0 / radius;
+  if constexpr (!CL) {
+    const double w = P.w_n[jh];
+    const bool eq = (jn_of(P, jh) == js_of(P, jh));
+    double* xm = x + (size_t)m * xl.mstride;
+    for (int r = threadIdx.x; r <= P.R; r += blockDim.x)
+      swe_out_g5(rings, cf, P, xm, xl, r, jh, w, w * ic2, ia, 2.0 * omega * mu, c2o, eq);
+  } else {
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    GRID_STAMP(5);
+    const int c = (int)cl.block_rank();
+    const int jb0 = jh - c;
+    const int nr = P.R + 1, r_lo = c * nr / 4, r_hi = (c + 1) * nr / 4;
+    double* xm = x + (size_t)m * xl.mstride;
+    for (int idx = threadIdx.x; idx < (r_hi - r_lo) * 4; idx += blockDim.x) {
+      const int i = idx & 3, r = r_lo + (idx >> 2);
+      const int jhi = jb0 + i;
+      const double mui = P.mu_n[jhi], wi = P.w_n[jhi];
+      const double2* ri = cl.map_shared_rank(rings, i);
+      const double2* ci = cl.map_shared_rank(cf, i);
+      swe_out_g5(ri, ci, P, xm, xl, r, jhi, wi, wi / (1.0 - mui * mui), ia, 2.0 * omega * mui, c2o,
+                 jn_of(P, jhi) == js_of(P, jhi));
+    }
+    GRID_STAMP(6);
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+    GRID_STAMP(7);
+  }
+}
+
 // Split SWE grid stage, second kernel (register FFTs): the 5 grids come from
 // HBM/L2 (written by f2g_reg_kernel); CTA (pair, member, role) stages the grid
 // rows it needs with async copies, each warp forms one product ring in
@@ -1155,6 +1335,22 @@ int swe_reg_launch(const PlanDev& P, const double2* eo, long long eo_mstride, do
   if (gridDim.x == 0) return kOk;
   static const int cl_knob = env_int("SWSDC_SWE_CLUSTER", 1);
   const bool cl = cl_knob && (jh_begin % 4 == 0) && ((jh_end - jh_begin) % 4 == 0);
+  static const int g5 = env_int("SWSDC_SWE_G5", 1);   // 0: the 12-FFT kernel below
+  if (NONLIN && g5) {
+    const size_t smem5 = sizeof(double2) * ((size_t)kG5Rings * P.ring_stride + 8 * (P.R + 1));
+    StageScope sc("swe_grid", st);
+    if (cl) {
+      SW_TRY(set_smem((const void*)swe_grid5_kernel<K, true>, smem5));
+      SW_CUDA(launch_pdl_cluster(swe_grid5_kernel<K, true>, dim3(gridDim), dim3(kG5Threads), smem5,
+                                 st, 4, P, eo, eo_mstride, x, xl, omega, radius, jh_begin));
+    } else {
+      SW_TRY(set_smem((const void*)swe_grid5_kernel<K, false>, smem5));
+      SW_CUDA(launch_pdl(swe_grid5_kernel<K, false>, dim3(gridDim), dim3(kG5Threads), smem5, st, P,
+                         eo, eo_mstride, x, xl, omega, radius, jh_begin));
+    }
+    SW_LAUNCH_CHECK();
+    return kOk;
+  }
   // warps: 6 for K >= 20 (registers), 7 for K = 16 (all forward FFTs in one round), 8 below
   const int threads = K >= 20 ? 192 : K == 16 ? 224 : 256;
   if (cl) {
