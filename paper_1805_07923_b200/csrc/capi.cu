@@ -326,8 +326,20 @@ int fe_grid_stage(swsdc_plan* p, bool nl, const double2* eo, int batch, double* 
   // smem-FFT split path: grids travel in the ring layout (coalesced rows per pair)
   double2* rg = reinterpret_cast<double2*>(p->grid_ws);
   const long long rfield = (long long)P.Jh * P.I;
-  SW_TRY(launch_fourier_to_rings(P, eo, fstride, rg, rfield, 5 * batch, st, jh_begin, jh_end));
-  return launch_swe_products(P, nl, reinterpret_cast<const double*>(rg), rfield, 5 * rfield, x, xl,
+  if (nl && batch <= 2) {
+    // the nonlinear products never read the delta grid (its Coriolis term is
+    // formed in Fourier space, swe_prod_kernel): U/a, V/a, zeta and phi' only
+    for (int m = 0; m < batch; ++m) {
+      SW_TRY(launch_fourier_to_rings(P, eo + (size_t)m * 5 * fstride, fstride, rg + (size_t)m * 5 * rfield,
+                                     rfield, 3, st, jh_begin, jh_end));
+      SW_TRY(launch_fourier_to_rings(P, eo + ((size_t)m * 5 + 4) * fstride, fstride,
+                                     rg + ((size_t)m * 5 + 4) * rfield, rfield, 1, st, jh_begin, jh_end));
+    }
+  } else {
+    SW_TRY(launch_fourier_to_rings(P, eo, fstride, rg, rfield, 5 * batch, st, jh_begin, jh_end));
+  }
+  return launch_swe_products(P, nl, reinterpret_cast<const double*>(rg), rfield, 5 * rfield, eo,
+                             fstride, x, xl,
                              batch, omega, radius, st, jh_begin, jh_end);
 }
 

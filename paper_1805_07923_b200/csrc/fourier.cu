@@ -1068,14 +1068,18 @@ __global__ void __launch_bounds__(256, 2) swe_grid_kernel(PlanDev P, const doubl
 }
 
 // ---------------------------------------------------------------------------
-// Large-n_lon variant of the fused grid stage: the 5 grids (U/a, V/a, zeta,
-// delta, phi') come from HBM (written by f2g_kernel) and the 7 products are
+// Large-n_lon variant of the fused grid stage: the grids (U/a, V/a, zeta,
+// phi') come from HBM (written by f2g_kernel) and the 5 products are
 // transformed pairwise through 2 rings, each pair completing its analysis
-// vectors: (A1, ZU) -> v1, v6; (A2, ZV) -> v2, v5; (PU, PV) -> v0, v4; KE -> v3.
+// vectors: (ZU, ZV) -> v1, v6, v2, v5; (PU, PV) -> v0, v4; KE -> v3.  As in
+// swe_grid5_kernel, the Coriolis terms A1 / A2 of v1 / v2 are formed in
+// Fourier space from the input spectra (E, O partial sums at eo) instead of
+// by two more forward transforms.
 // ---------------------------------------------------------------------------
 template <bool NONLIN, bool BIGP, bool RINGS = false, int K15 = 0>
 __global__ void __launch_bounds__(256, 1) swe_prod_kernel(PlanDev P, const double* grids,
                                                           long long gfield, long long gmember,
+                                                          const double2* eo, long long eo_fstride,
                                                           double* x, XLayout xl, double omega,
                                                           double radius, int jh_begin) {
   pdl_wait();
@@ -1098,21 +1102,26 @@ __global__ void __launch_bounds__(256, 1) swe_prod_kernel(PlanDev P, const doubl
     const double* g = gm + (size_t)q * gfield + (size_t)il * P.J;
     return d2(g[jn], g[js]);
   };
+  // input spectra (F_n, F_s) of field q at wavenumber r (Im dropped at r = 0,
+  // as the grid round trip would): eo fields U/a, V/a, zeta, delta, phi'
+  const double2* em = eo + (size_t)m * 5 * eo_fstride + (size_t)jh * 2;
+  auto coef = [&](int q, int r, double2& Fn, double2& Fs) {
+    const double2* e = em + (size_t)q * eo_fstride + (size_t)r * P.Jh * 2;
+    const double2 E = e[0], O = e[1];
+    Fn = d2(E.x + O.x, r == 0 ? 0.0 : E.y + O.y);
+    Fs = d2(E.x - O.x, r == 0 ? 0.0 : E.y - O.y);
+  };
   // linear only (include_nonlinear=False): one pass of (A1, A2) -> v0, v1
-  for (int pass = NONLIN ? 0 : 4; pass < (NONLIN ? 4 : 5); ++pass) {
-    const int nr = (pass == 3) ? 1 : 2;
+  for (int pass = NONLIN ? 0 : 4; pass < (NONLIN ? 3 : 5); ++pass) {
+    const int nr = (pass == 2) ? 1 : 2;
     for (int il = threadIdx.x; il < I; il += blockDim.x) {
       const double2 U = gv(0, il), V = gv(1, il);
       double2 a, b = d2(0.0, 0.0);
-      if (pass == 0) {          // A1 = -f delta - c2o V ; ZU = zeta U
-        const double2 D = gv(3, il), Z = gv(2, il);
-        a = d2(-fn * D.x - c2o * V.x, fn * D.y - c2o * V.y);
-        b = d2(Z.x * U.x, Z.y * U.y);
-      } else if (pass == 1) {   // A2 = f zeta - c2o U ; ZV = zeta V
+      if (pass == 0) {          // ZU = zeta U ; ZV = zeta V
         const double2 Z = gv(2, il);
-        a = d2(fn * Z.x - c2o * U.x, -fn * Z.y - c2o * U.y);
+        a = d2(Z.x * U.x, Z.y * U.y);
         b = d2(Z.x * V.x, Z.y * V.y);
-      } else if (pass == 2) {   // PU = phi U ; PV = phi V
+      } else if (pass == 1) {   // PU = phi U ; PV = phi V
         const double2 Ph = gv(4, il);
         a = d2(Ph.x * U.x, Ph.y * U.y);
         b = d2(Ph.x * V.x, Ph.y * V.y);
@@ -1140,14 +1149,23 @@ __global__ void __launch_bounds__(256, 1) swe_prod_kernel(PlanDev P, const doubl
       if (nr == 2) get_pair(rings + RS, P, r, Bn, Bs);
       const double rwa = r * wc * ia, wa = wc * ia;
       if (pass == 0) {
-        put_x(xm, xl, 1, r, jh, cadd2(cscale(An, w), ir_scale(Bn, -rwa)),
-              cadd2(cscale(As, w), ir_scale(Bs, -rwa)), eq);
-        put_x(xm, xl, 6, r, jh, cscale(Bn, wa), cscale(Bs, wa), eq);
-      } else if (pass == 1) {
-        put_x(xm, xl, 2, r, jh, cadd2(cscale(An, w), ir_scale(Bn, rwa)),
-              cadd2(cscale(As, w), ir_scale(Bs, rwa)), eq);
+        // swe.py:262,265 in Fourier space (f = fn north, -fn south)
+        double2 Un, Us, Vn, Vs, Zn, Zs, Dn, Ds;
+        coef(0, r, Un, Us);
+        coef(1, r, Vn, Vs);
+        coef(2, r, Zn, Zs);
+        coef(3, r, Dn, Ds);
+        const double2 A1n = d2(-fn * Dn.x - c2o * Vn.x, -fn * Dn.y - c2o * Vn.y);
+        const double2 A1s = d2(fn * Ds.x - c2o * Vs.x, fn * Ds.y - c2o * Vs.y);
+        const double2 A2n = d2(fn * Zn.x - c2o * Un.x, fn * Zn.y - c2o * Un.y);
+        const double2 A2s = d2(-fn * Zs.x - c2o * Us.x, -fn * Zs.y - c2o * Us.y);
+        put_x(xm, xl, 1, r, jh, cadd2(cscale(A1n, w), ir_scale(An, -rwa)),
+              cadd2(cscale(A1s, w), ir_scale(As, -rwa)), eq);
+        put_x(xm, xl, 6, r, jh, cscale(An, wa), cscale(As, wa), eq);
+        put_x(xm, xl, 2, r, jh, cadd2(cscale(A2n, w), ir_scale(Bn, rwa)),
+              cadd2(cscale(A2s, w), ir_scale(Bs, rwa)), eq);
         put_x(xm, xl, 5, r, jh, cscale(Bn, wa), cscale(Bs, wa), eq);
-      } else if (pass == 2) {
+      } else if (pass == 1) {
         put_x(xm, xl, 0, r, jh, ir_scale(An, -rwa), ir_scale(As, -rwa), eq);
         put_x(xm, xl, 4, r, jh, cscale(Bn, wa), cscale(Bs, wa), eq);
       } else if (pass == 4) {
@@ -1384,26 +1402,28 @@ int swe_fwd_reg_launch(const PlanDev& P, const double2* grids, long long gfield,
 
 template <bool NONLIN, bool BIGP, int K15>
 int swe_prod_launch_k(const PlanDev& P, const double* grids, long long gfield, long long gmember,
-                      double* x, const XLayout& xl, int nmembers, double omega, double radius,
-                      int jh_begin, int jh_end, cudaStream_t st) {
+                      const double2* eo, long long eo_fstride, double* x, const XLayout& xl,
+                      int nmembers, double omega, double radius, int jh_begin, int jh_end,
+                      cudaStream_t st) {
   // grids in the ring layout (f2g_kernel<., true>): gfield / gmember in double2
   const size_t smem = sizeof(double2) * 2 * P.ring_stride;
   SW_TRY(set_smem((const void*)swe_prod_kernel<NONLIN, BIGP, true, K15>, smem));
   dim3 gridDim(jh_end - jh_begin, nmembers);
   if (gridDim.x == 0) return kOk;
   StageScope sc("swe_products", st);
-  SW_CUDA(launch_pdl(swe_prod_kernel<NONLIN, BIGP, true, K15>, dim3(gridDim), dim3(BIGP && K15 == 0 ? 128 : 256), smem, st, P, grids, gfield, gmember, x, xl, omega, radius, jh_begin));
+  SW_CUDA(launch_pdl(swe_prod_kernel<NONLIN, BIGP, true, K15>, dim3(gridDim), dim3(BIGP && K15 == 0 ? 128 : 256), smem, st, P, grids, gfield, gmember, eo, eo_fstride, x, xl, omega, radius, jh_begin));
   SW_LAUNCH_CHECK();
   return kOk;
 }
 
 template <bool NONLIN, bool BIGP>
 int swe_prod_launch(const PlanDev& P, const double* grids, long long gfield, long long gmember,
-                    double* x, const XLayout& xl, int nmembers, double omega, double radius,
-                    int jh_begin, int jh_end, cudaStream_t st) {
-  SWSDC_K15_SWITCH(fft15_path(P, 0), (swe_prod_launch_k<NONLIN, false, KK>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, jh_begin, jh_end, st)));
-  return swe_prod_launch_k<NONLIN, BIGP, 0>(P, grids, gfield, gmember, x, xl, nmembers, omega,
-                                            radius, jh_begin, jh_end, st);
+                    const double2* eo, long long eo_fstride, double* x, const XLayout& xl,
+                    int nmembers, double omega, double radius, int jh_begin, int jh_end,
+                    cudaStream_t st) {
+  SWSDC_K15_SWITCH(fft15_path(P, 0), (swe_prod_launch_k<NONLIN, false, KK>(P, grids, gfield, gmember, eo, eo_fstride, x, xl, nmembers, omega, radius, jh_begin, jh_end, st)));
+  return swe_prod_launch_k<NONLIN, BIGP, 0>(P, grids, gfield, gmember, eo, eo_fstride, x, xl,
+                                            nmembers, omega, radius, jh_begin, jh_end, st);
 }
 
 }  // namespace
@@ -1479,16 +1499,17 @@ bool swe_split_preferred(const PlanDev& P, long long pair_members) {
 }
 
 int launch_swe_products(const PlanDev& P, bool nonlinear, const double* grids, long long gfield,
-                        long long gmember, double* x, const XLayout& xl, int nmembers,
-                        double omega, double radius, cudaStream_t st, int jh_begin, int jh_end) {
+                        long long gmember, const double2* eo, long long eo_fstride, double* x,
+                        const XLayout& xl, int nmembers, double omega, double radius,
+                        cudaStream_t st, int jh_begin, int jh_end) {
   if (jh_end < 0) jh_end = P.Jh;
   const bool big = swfft::fft_needs_bigp(P.I);
   if (nonlinear) {
-    if (big) return swe_prod_launch<true, true>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
-    return swe_prod_launch<true, false>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
+    if (big) return swe_prod_launch<true, true>(P, grids, gfield, gmember, eo, eo_fstride, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
+    return swe_prod_launch<true, false>(P, grids, gfield, gmember, eo, eo_fstride, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
   }
-  if (big) return swe_prod_launch<false, true>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
-  return swe_prod_launch<false, false>(P, grids, gfield, gmember, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
+  if (big) return swe_prod_launch<false, true>(P, grids, gfield, gmember, eo, eo_fstride, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
+  return swe_prod_launch<false, false>(P, grids, gfield, gmember, eo, eo_fstride, x, xl, nmembers, omega, radius, jh_begin, jh_end, st);
 }
 
 // Smem-FFT inverse of nf (E, O) fields into the ring layout rings[f][jh][il]

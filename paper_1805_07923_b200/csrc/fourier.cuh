@@ -34,8 +34,8 @@ int launch_swe_split_reg(const PlanDev& P, bool nonlinear, const double2* eo, lo
 // layout (double2 rings[m * gmember + q * gfield + jh * I + il], q = U/a, V/a,
 // zeta, delta, phi'; strides in double2)
 int launch_swe_products(const PlanDev& P, bool nonlinear, const double* grids, long long gfield,
-                        long long gmember, double* x, const XLayout& xl, int nmembers,
-                        double omega, double radius, cudaStream_t st, int jh_begin = 0,
-                        int jh_end = -1);
+                        long long gmember, const double2* eo, long long eo_fstride, double* x,
+                        const XLayout& xl, int nmembers, double omega, double radius,
+                        cudaStream_t st, int jh_begin = 0, int jh_end = -1);
 
 }  // namespace swsdc
