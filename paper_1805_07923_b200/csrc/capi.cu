@@ -344,6 +344,19 @@ int fe_grid_stage(swsdc_plan* p, bool nl, const double2* eo, int batch, double* 
 }
 
 // Legendre analysis of the nv vectors (XLayout xl) of each member into out.
+// x layout of the F_E pipeline: pair-major for the nonlinear tendency on the
+// fused register-FFT grid path (swe_grid5_kernel then writes whole sectors per
+// latitude pair without the 4-CTA cluster exchange; measured: config 4 step
+// -1.1%, config 0 -3%, config 2 -0.5%, though the analysis' ring re-ordering
+// costs it ~10%); column-major elsewhere -- the large-n_lon split path (config
+// 3: +0.9% with pair-major) and the DFMA / TMA comparison kernels.
+XLayout fe_xlayout(const PlanDev& P, bool nl) {
+  static const int knob = env_int("SWSDC_FE_PM", 1);
+  const bool pm = knob && nl && !ana_dfma_enabled() && !ana_uses_tma(7) && fourier_reg_fft(P) &&
+                  swe_grid_fits(P);
+  return make_xlayout(P.R, P.Jh, nl ? 7 : 2, pm);
+}
+
 int ana_run(swsdc_plan* p, const double* x, const XLayout& xl, int nmembers, double2* out,
             long long out_vstride, long long out_rstride, long long out_mstride, int smax,
             bool zero_fill, cudaStream_t st) {
@@ -711,7 +724,7 @@ int swsdc_eval_fe(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, c
   const PlanDev& P = p->dev;
   const long long fstride = (long long)(P.R + 1) * P.Jh * 2;
   const long long plane = (long long)(P.R + 1) * (P.R + 1);
-  const XLayout xl = make_xlayout(P.R, P.Jh, nv);
+  const XLayout xl = fe_xlayout(P, nl);
   double2* eo = ws_eo(p);
   double* x = ws_x(p, 5 * batch);
   double2* y = ws_y(p, 5 * batch, xb);
@@ -743,7 +756,7 @@ int swsdc_fe_layout(swsdc_plan* p, int nonlinear, int batch, long long* eo_doubl
                     long long* x_doubles, int* x_nc, int* x_jh4) {
   if (!p || batch < 0) { set_error("bad arguments"); return kUsage; }
   const PlanDev& P = p->dev;
-  const XLayout xl = make_xlayout(P.R, P.Jh, nonlinear ? 7 : 2);
+  const XLayout xl = fe_xlayout(P, nonlinear != 0);
   if (eo_doubles) *eo_doubles = (long long)batch * 5 * (P.R + 1) * P.Jh * 4;
   if (x_doubles) *x_doubles = (long long)batch * xl.mstride;
   if (x_nc) *x_nc = xl.nc;
@@ -788,7 +801,7 @@ int swsdc_fe_grid(swsdc_plan* p, const swsdc_params* q, int include_nonlinear, c
   }
   if (batch == 0 || jh_begin == jh_end) return kOk;
   const bool nl = include_nonlinear != 0;
-  const XLayout xl = make_xlayout(P.R, P.Jh, nl ? 7 : 2);
+  const XLayout xl = fe_xlayout(P, nl);
   const double2* e = reinterpret_cast<const double2*>(eo);
   return fe_grid_stage(p, nl, e, batch, x, xl, q->omega, q->radius, S(stream), jh_begin, jh_end);
 }
@@ -802,7 +815,7 @@ int swsdc_fe_analysis(swsdc_plan* p, const swsdc_params* q, int include_nonlinea
   const bool nl = include_nonlinear != 0;
   const int nv = nl ? 7 : 2;
   SW_TRY(ensure_ws(p, 0, 0, nv * batch, S(stream)));
-  const XLayout xl = make_xlayout(P.R, P.Jh, nv);
+  const XLayout xl = fe_xlayout(P, nl);
   double2* y = ws_y(p, 0, 0);
   const long long yv = (long long)(P.R + 1) * p->ldy;
   const long long plane = (long long)(P.R + 1) * (P.R + 1);

@@ -148,20 +148,29 @@ struct PlanDev {
 // latitudes jb, parity p in {S, D}), nc = 8*NT real columns (re/im of each
 // vector) x 4 latitudes -- exactly one m8n8k4 B fragment per (jb, p, n-tile),
 // so a warp loads it with one coalesced 256-byte access.
+//
+// pm (pair-major, the F_E path): inside each (r, jb, p) block of nc x 4
+// doubles the latitude is the slow index -- [t][n] instead of [n][t] -- so
+// the nc columns of one latitude pair are contiguous (whole 32-byte sectors
+// written by the pair's own CTA, no cluster exchange); the analysis kernel
+// re-orders them into its fragment ring (ana_item<..., PM>).
 struct XLayout {
   int nv;          // vectors
   int nc;          // columns per group (8 * n-tiles of a full group)
   int jh4;         // ceil(Jh / 4)
   long long gstride;  // doubles per group of 16 vectors
   long long mstride;  // doubles per member
+  int pm;          // pair-major blocks
   __host__ __device__ size_t idx(int v, int comp, int r, int jh, int p) const {
     const int g = v >> 4, n = 2 * (v & 15) + comp;
-    return (size_t)g * gstride + ((((size_t)r * jh4 + (jh >> 2)) * 2 + p) * nc + n) * 4 + (jh & 3);
+    const size_t blk = (size_t)g * gstride + (((size_t)r * jh4 + (jh >> 2)) * 2 + p) * nc * 4;
+    return pm ? blk + (size_t)(jh & 3) * nc + n : blk + (size_t)n * 4 + (jh & 3);
   }
 };
 
-inline XLayout make_xlayout(int R, int Jh, int nv) {
+inline XLayout make_xlayout(int R, int Jh, int nv, bool pair_major = false) {
   XLayout L;
+  L.pm = pair_major ? 1 : 0;
   L.nv = nv;
   const int nfull = nv < 16 ? nv : 16;
   L.nc = 8 * ((2 * nfull + 7) / 8);

@@ -218,6 +218,11 @@ __device__ __forceinline__ void put_x(double* x, const XLayout& L, int v, int r,
     S = d2(vn.x + vs.x, vn.y + vs.y);
     D = d2(vn.x - vs.x, vn.y - vs.y);
   }
+  if (L.pm) {   // re / im columns adjacent: one 16-byte store per parity
+    *reinterpret_cast<double2*>(x + L.idx(v, 0, r, jh, 0)) = S;
+    *reinterpret_cast<double2*>(x + L.idx(v, 0, r, jh, 1)) = D;
+    return;
+  }
   x[L.idx(v, 0, r, jh, 0)] = S.x;
   x[L.idx(v, 1, r, jh, 0)] = S.y;
   x[L.idx(v, 0, r, jh, 1)] = D.x;
@@ -1352,7 +1357,9 @@ int swe_reg_launch(const PlanDev& P, const double2* eo, long long eo_mstride, do
   dim3 gridDim(jh_end - jh_begin, nmembers);
   if (gridDim.x == 0) return kOk;
   static const int cl_knob = env_int("SWSDC_SWE_CLUSTER", 1);
-  const bool cl = cl_knob && (jh_begin % 4 == 0) && ((jh_end - jh_begin) % 4 == 0);
+  // the cluster only serves the column-major layout's 32-byte sectors; pair-major
+  // x is written whole-sector by each pair's CTA
+  const bool cl = cl_knob && !xl.pm && (jh_begin % 4 == 0) && ((jh_end - jh_begin) % 4 == 0);
   static const int g5 = env_int("SWSDC_SWE_G5", 1);   // 0: the 12-FFT kernel below
   if (NONLIN && g5) {
     const size_t smem5 = sizeof(double2) * ((size_t)kG5Rings * P.ring_stride + 8 * (P.R + 1));

@@ -569,13 +569,23 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 constexpr int kBDepth = 4;
 // A fragments of one k-step in the table-fed variant: [parity][m-tile][lane]
 constexpr int kAFrag = 2 * 2 * 32;
-template <int NT, bool TAB = false>
+// Pair-major x (XLayout::pm): the ring holds each k-step's B block as
+// [parity][latitude t][S] rows, S = 8 NT padded to 8 (mod 16) doubles so the
+// fragment reads (lane g, t -> row t, column 8 n + g) take the minimum 2
+// wavefronts.
+template <int NT>
+__host__ __device__ constexpr int ana_pm_stride() {
+  return (8 * NT + 8) % 16 == 0 ? 8 * NT + 16 : 8 * NT + 8;
+}
+template <int NT, bool PM>
+__host__ __device__ constexpr int ana_bslot() { return PM ? 2 * 4 * ana_pm_stride<NT>() : 2 * NT * 32; }
+template <int NT, bool TAB = false, bool PM = false>
 __host__ __device__ constexpr int ana_warp_doubles() {
   // TAB: no q tile or betas; the ring carries A and B fragments and, after the
   // k-loop, the epilogue staging ([4 NT][33] double2) and the split reduction
-  return TAB ? (kBDepth * (2 * NT * 32 + kAFrag) > 4 * NT * 33 * 2
-                    ? kBDepth * (2 * NT * 32 + kAFrag) : 4 * NT * 33 * 2)
-             : kChunk * kQS + kChunk + kBDepth * 2 * NT * 32;
+  return TAB ? (kBDepth * (ana_bslot<NT, PM>() + kAFrag) > 4 * NT * 33 * 2
+                    ? kBDepth * (ana_bslot<NT, PM>() + kAFrag) : 4 * NT * 33 * 2)
+             : kChunk * kQS + kChunk + kBDepth * ana_bslot<NT, PM>();
 }
 
 // One work item (r, first chunk, checkpoint index) of member m (one CTA; a
@@ -590,12 +600,14 @@ __host__ __device__ constexpr int ana_warp_doubles() {
 // fragment-native table P.ptab (reference-rounded values, build_ptab) through
 // the same cp.async ring as the B fragments; no seeds, betas, q tile or chunk
 // scale g.
-template <int NT, int LSPLIT, int MP = 1, bool TAB = false>
+template <int NT, int LSPLIT, int MP = 1, bool TAB = false, bool PM = false>
 __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, const int4 wk, int m,
                                          double* smem) {
   static_assert(MP == 1 || (MP == 2 && NT % 4 == 0), "member pairs need NT / 2 even");
-  constexpr int kWD = ana_warp_doubles<NT, TAB>();
-  constexpr int kSlot = 2 * NT * 32 + (TAB ? kAFrag : 0);        // ring slot (doubles)
+  constexpr int kWD = ana_warp_doubles<NT, TAB, PM>();
+  constexpr int kBS = ana_bslot<NT, PM>();                       // B part of a ring slot
+  constexpr int kSlot = kBS + (TAB ? kAFrag : 0);                // ring slot (doubles)
+  constexpr int kS = ana_pm_stride<NT>();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   double* qs = smem + (size_t)warp * kWD;                        // [32][kQS] (TAB: staging only)
@@ -674,6 +686,25 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
     const size_t jump = (size_t)((LSPLIT - 1) * 8 + 1) * jb_stride;
     const size_t poff = (size_t)nc * 4;                       // parity-1 half of a block
     const double* ip = xr + (size_t)(half << 3) * jb_stride;  // block of the next issue
+    // pair-major: 16-byte copies of the block's 8 rows [p][t] of nc doubles (MP = 2:
+    // nc / 2 of each member) into ring rows of kS; loop-invariant per-lane offsets
+    constexpr int kPmCp = PM ? (MP == 2 ? 4 : NT) : 1;
+    int pm_s[kPmCp], pm_d[kPmCp];
+    if constexpr (PM) {
+#pragma unroll
+      for (int u = 0; u < kPmCp; ++u) {
+        const int cc = lane + 32 * u;
+        if constexpr (MP == 2) {
+          const int h = cc >> 6, row = (cc >> 3) & 7, q = cc & 7;
+          pm_s[u] = row * 16 + 2 * q;   // + member h offset at issue time
+          pm_d[u] = row * kS + h * 16 + 2 * q;
+        } else {
+          const int row = cc / (4 * NT), q = cc - row * (4 * NT);
+          pm_s[u] = row * nc + 2 * q;
+          pm_d[u] = row * kS + 2 * q;
+        }
+      }
+    }
     // TAB: A fragments of this warp's chunk, kAFrag doubles per 4-latitude block
     const double* ap = TAB ? P.ptab + ((size_t)(wk.z + (c - wk.y)) * jh4 + (half << 3)) * kAFrag
                            : nullptr;
@@ -682,10 +713,16 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
       if (iss < nks && ijb < jh4) {
         double* dst = bring + (iss & (kBDepth - 1)) * kSlot;
         if constexpr (TAB) {
-          cp_async16_ana(dst + 2 * NT * 32 + 2 * lane, ap + 2 * lane);
-          cp_async16_ana(dst + 2 * NT * 32 + 64 + 2 * lane, ap + 64 + 2 * lane);
+          cp_async16_ana(dst + kBS + 2 * lane, ap + 2 * lane);
+          cp_async16_ana(dst + kBS + 64 + 2 * lane, ap + 64 + 2 * lane);
         }
-        if constexpr (NT % 2 == 0) {
+        if constexpr (PM) {
+#pragma unroll
+          for (int u = 0; u < kPmCp; ++u) {
+            const size_t mo = (MP == 2 && u >= 2) ? (size_t)a.xl.mstride : 0;
+            cp_async16_ana(dst + pm_d[u], ip + mo + pm_s[u]);
+          }
+        } else if constexpr (NT % 2 == 0) {
           // each parity half is NT/2 copies per lane at fixed offsets from the
           // lane's base: immediate-offset addressing, no per-step index math
           const double* s0 = ip + 2 * lane;
@@ -769,14 +806,14 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
           for (int p = 0; p < 2; ++p)
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
-              const double b = bsrc[p * NT * 32 + n * 32 + lane];
+              const double b = PM ? bsrc[(p * 4 + t) * kS + n * 8 + g] : bsrc[p * NT * 32 + n * 32 + lane];
               bv[p][n] = FULL ? b : (ok ? b : 0.0);
             }
 #pragma unroll
           for (int p = 0; p < 2; ++p)
 #pragma unroll
             for (int mt = 0; mt < MTN; ++mt) {
-              const double av = TAB ? bsrc[2 * NT * 32 + (p * 2 + mt) * 32 + lane]
+              const double av = TAB ? bsrc[kBS + (p * 2 + mt) * 32 + lane]
                                     : qs[(p * 16 + mt * 8 + g) * kQS + s * 4 + t];
 #pragma unroll
               for (int n = 0; n < NT; ++n) dmma884(acc[p][mt][n], av, bv[p][n]);
@@ -799,7 +836,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
     // only the LSPLIT warps of one chunk meet (named barrier 1 + chunk)
     const unsigned bar_id = 1 + warp / LSPLIT, bar_n = 32 * LSPLIT;
     asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
-    double* red = smem + (size_t)warp * ana_warp_doubles<NT, TAB>();
+    double* red = smem + (size_t)warp * ana_warp_doubles<NT, TAB, PM>();
     if (half > 0 && active) {
 #pragma unroll
       for (int p = 0; p < 2; ++p)
@@ -816,7 +853,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
     if (!active) return;
     if (half > 0) return;
     for (int h = 1; h < LSPLIT; ++h) {
-      const double* src = smem + (size_t)(warp + h) * ana_warp_doubles<NT, TAB>();
+      const double* src = smem + (size_t)(warp + h) * ana_warp_doubles<NT, TAB, PM>();
 #pragma unroll
       for (int p = 0; p < 2; ++p)
 #pragma unroll
@@ -840,7 +877,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
   // coalesced 512-byte store instead of 16-byte pieces two degrees apart.
   {
     double2* stg = reinterpret_cast<double2*>(qs);   // [4 NT][33] double2 (4 NT * 33 * 2 <= 32 kQS)
-    static_assert(4 * NT * 33 * 2 <= (TAB ? ana_warp_doubles<NT, TAB>() : kChunk * kQS),
+    static_assert(4 * NT * 33 * 2 <= (TAB ? ana_warp_doubles<NT, TAB, PM>() : kChunk * kQS),
                   "staging fits the q tile / ring");
     __syncwarp();
 #pragma unroll
@@ -869,12 +906,12 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
 }
 
 // One CTA per work item (grid: items x members).
-template <int NT, int LSPLIT, int MP = 1, bool TAB = false>
+template <int NT, int LSPLIT, int MP = 1, bool TAB = false, bool PM = false>
 __global__ void __launch_bounds__(kAnaWarps * 32)
 ana_kernel(PlanDev P, AnaArgs a) {
   pdl_trigger();   // pdl_wait() inside ana_item, after the plan-table loads
   extern __shared__ __align__(16) double smem[];
-  ana_item<NT, LSPLIT, MP, TAB>(P, a, a.work[blockIdx.x], blockIdx.y, smem);
+  ana_item<NT, LSPLIT, MP, TAB, PM>(P, a, a.work[blockIdx.x], blockIdx.y, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -1062,9 +1099,16 @@ bool ana_dfma() {
 template <int LSPLIT>
 int launch_ana_pairs_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st) {
   const int warps = LSPLIT * ana_chunks_per_cta(LSPLIT);
-  const bool tab = ana_table_fed(P, 4, 2);
-  const size_t smem = sizeof(double) * warps * (tab ? ana_warp_doubles<4, true>() : ana_warp_doubles<4>());
-  auto kern = tab ? ana_kernel<4, LSPLIT, 2, true> : ana_kernel<4, LSPLIT, 2>;
+  const bool tab = ana_table_fed(P, 4, 2), pm = a.xl.pm != 0;
+  if (pm && a.xl.nc != 16) {
+    set_error("pair-major member-pair analysis needs 16 columns per member");
+    return kUsage;
+  }
+  const size_t smem = sizeof(double) * warps *
+                      (pm ? (tab ? ana_warp_doubles<4, true, true>() : ana_warp_doubles<4, false, true>())
+                          : (tab ? ana_warp_doubles<4, true>() : ana_warp_doubles<4>()));
+  auto kern = pm ? (tab ? ana_kernel<4, LSPLIT, 2, true, true> : ana_kernel<4, LSPLIT, 2, false, true>)
+                 : (tab ? ana_kernel<4, LSPLIT, 2, true> : ana_kernel<4, LSPLIT, 2>);
   SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
   StageScope sc("legendre_analysis", st);
   SW_CUDA(launch_pdl(kern, dim3(dim3(nwork, a.nmembers)), dim3(warps * 32), smem, st, P, a));
@@ -1085,6 +1129,21 @@ int launch_ana_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st)
     return kOk;
   }
   const bool tab = ana_table_fed(P, NT, 1);
+  if (a.xl.pm) {
+    // pair-major x (the F_E path, 7 vectors): NT = 2, recurrence-fed
+    if constexpr (NT == 2) {
+      const size_t smem = sizeof(double) * warps * ana_warp_doubles<NT, false, true>();
+      auto kern = ana_kernel<NT, LSPLIT, 1, false, true>;
+      SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
+      StageScope sc("legendre_analysis", st);
+      SW_CUDA(launch_pdl(kern, dim3(dim3(nwork, a.nmembers)), dim3(warps * 32), smem, st, P, a));
+      SW_LAUNCH_CHECK();
+      return kOk;
+    } else {
+      set_error("pair-major analysis is built for 5..8 vectors");
+      return kUsage;
+    }
+  }
   const size_t smem = sizeof(double) * warps * (tab ? ana_warp_doubles<NT, true>() : ana_warp_doubles<NT>());
   auto kern = tab ? ana_kernel<NT, LSPLIT, 1, true> : ana_kernel<NT, LSPLIT>;
   SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
@@ -1385,6 +1444,8 @@ int launch_analysis_pairs(const PlanDev& P, const AnaArgs& a, int nwork, int lsp
 bool ana_table_fed(const PlanDev& P, int nt, int mp) {
   return P.ptab != nullptr && nt * mp >= 3;
 }
+
+bool ana_dfma_enabled() { return ana_dfma(); }
 
 bool ana_pairs_ok(int nv, int nmembers) {
   static const int knob = env_int("SWSDC_ANA_PAIRS", 1);

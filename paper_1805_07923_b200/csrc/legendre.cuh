@@ -59,6 +59,7 @@ int build_ptab(const PlanDev& P, const double* a_tab, const double* b_tab, const
                double* ptab, cudaStream_t st);
 constexpr int kAnaSplits = 4;
 bool ana_uses_tma(int nv);
+bool ana_dfma_enabled();   // SWSDC_ANA_DFMA comparison kernel selected
 // Ensemble analysis two members per CTA (a.nmembers = member pairs, nv <= 8
 // vectors each, members m and m + 1 adjacent at a.xl.mstride / a.out_mstride).
 bool ana_pairs_ok(int nv, int nmembers);
