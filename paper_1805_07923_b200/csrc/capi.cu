@@ -168,6 +168,23 @@ int syn_plain(swsdc_plan* p, const double2* coeffs, int r_in, int batch, double2
   for (int cand = 6; cand >= 4 && !B; --cand)
     if (batch % cand == 0) { B = cand; break; }
   int done = 0;
+  // wide batches on the tensor cores (opt-in, SWSDC_SYN_DMMA=1: 31.3 vs 29.1 us for the
+  // DFMA kernel at config 1 -- with 16 fields per CTA only 128 CTAs, with 8 the shared
+  // coefficient tiles and table stream still leave the DMMA pipe latency-bound)
+  while (P.stab && batch - done >= 8) {
+    const int nf = std::min(16, batch - done);
+    SynArgs a{};
+    a.src = coeffs + done * cin;
+    a.src_fstride = cin;
+    a.src_R = r_in;
+    a.smax = P.R;
+    a.eo = eo + done * fstride;
+    a.src_mstride = cin * nf;
+    a.eo_mstride = fstride * nf;
+    a.nmembers = 1;
+    SW_TRY(launch_synthesis_dmma(P, a, nf, st));
+    done += nf;
+  }
   while (done < batch) {
     int b = B;
     int groups;
@@ -570,6 +587,22 @@ int swsdc_plan_create(int R, int n_lon, int n_lat, const double* mu, const doubl
         p->owned.push_back(tb);
         P.ptab = reinterpret_cast<const double*>(tb);
         st = build_ptab(P, d_a, d_b, d_sect, reinterpret_cast<double*>(tb), 0);
+      }
+    }
+    // the synthesis-order table of the tensor-core synthesis (wide plain batches;
+    // opt-in comparison, SWSDC_SYN_DMMA=1: measured slower than the DFMA kernel)
+    static const int syn_dmma = env_int("SWSDC_SYN_DMMA", 0);
+    const size_t stab_bytes = sizeof(double) * 8 * 128 * (size_t)nck * ((P.Jh + 31) / 32);
+    if (st == kOk && tables && syn_dmma && P.Jh <= 256 &&
+        stab_bytes <= (size_t)cap_mb * 1024 * 1024) {
+      void* tb = nullptr;
+      if (cudaMalloc(&tb, stab_bytes) != cudaSuccess || cudaMemset(tb, 0, stab_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        if (tb) cudaFree(tb);
+      } else {
+        p->owned.push_back(tb);
+        P.stab = reinterpret_cast<const double*>(tb);
+        st = build_ptab(P, d_a, d_b, d_sect, reinterpret_cast<double*>(tb), 0, 1);
       }
     }
   }

@@ -137,6 +137,7 @@ struct PlanDev {
   const double2* ckpt;    // [sum_r nchunk(r)][Jh] (q_{s0}, q_{s0+1}) chunk seeds
   const int* ck_off;      // [R+1] first chunk index of row r in ckpt
   const double* ptab;     // [nck][jh4][128] Pbar A fragments (table-fed analysis) or nullptr
+  const double* stab;     // [nck][ceil(Jh/32)][8][128] Pbar B fragments (tensor-core synthesis) or nullptr
   const double2* tw;      // [I] exp(-2 pi i e / I)
   const int* rev;         // [I] padded ring slot of frequency k (digit-reversed DIF order)
   int ring_stride;        // double2 slots per ring in shared memory (== 1 mod 8)

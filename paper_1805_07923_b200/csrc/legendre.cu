@@ -100,7 +100,7 @@ int build_checkpoints(const PlanDev& P, const double* a_tab, const double* b_tab
 // R+1 or Jh stay zero (the buffer is zeroed first).
 // ---------------------------------------------------------------------------
 __global__ void build_ptab_kernel(PlanDev P, const double* a_tab, const double* b_tab,
-                                  const double* sect_fac, double* ptab) {
+                                  const double* sect_fac, double* ptab, int syn) {
   pdl_wait();
   pdl_trigger();
   const int jh = blockIdx.x * blockDim.x + threadIdx.x;
@@ -113,7 +113,7 @@ __global__ void build_ptab_kernel(PlanDev P, const double* a_tab, const double* 
   const double* ar = a_tab + (size_t)r * P.ldk;
   const double* br = b_tab + (size_t)r * P.ldk;
   const int jh4 = (P.Jh + 3) >> 2, jb = jh >> 2, tt = jh & 3;
-  const size_t base = (size_t)P.ck_off[r] * jh4;
+  const int nlb = (P.Jh + 31) >> 5, lb = jh >> 5, lt = (jh >> 3) & 3, gg = jh & 7;
   double pm1 = 0.0, pm2 = 0.0;
   for (int k = 0; k <= P.R + 1 - r; ++k) {
     double pk;
@@ -121,19 +121,26 @@ __global__ void build_ptab_kernel(PlanDev P, const double* a_tab, const double* 
     else if (k == 1) pk = __dmul_rn(__dmul_rn(mu, ar[1]), sect);
     else pk = __dsub_rn(__dmul_rn(__dmul_rn(ar[k], mu), pm1), __dmul_rn(br[k], pm2));
     const int c = k >> 5, kk = k & 31, pp = kk & 1, i = kk >> 1;
-    const int lane = ((i & 7) << 2) | tt;
-    ptab[((base + (size_t)c * jh4 + jb) << 7) + ((pp << 1) | (i >> 3)) * 32 + lane] = pk;
+    const size_t ck = (size_t)P.ck_off[r] + c;
+    if (!syn) {
+      // analysis A fragment: [p][m-tile i/8][lane = 4 (i%8) + t], latitude t of block jb
+      const int lane = ((i & 7) << 2) | tt;
+      ptab[((ck * jh4 + jb) << 7) + ((pp << 1) | (i >> 3)) * 32 + lane] = pk;
+    } else {
+      // synthesis B fragment: k-step (p, q = i/4), latitude tile lt, lane = 4 g + (i%4)
+      ptab[(((ck * nlb + lb) * 8 + (pp * 4 + (i >> 2))) << 7) + lt * 32 + (gg << 2) + (i & 3)] = pk;
+    }
     pm2 = pm1;
     pm1 = pk;
   }
 }
 
 int build_ptab(const PlanDev& P, const double* a_tab, const double* b_tab, const double* sect_fac,
-               double* ptab, cudaStream_t st) {
+               double* ptab, cudaStream_t st, int syn) {
   const int threads = 64;
   StageScope sc("build_ptab", st);
   SW_CUDA(launch_pdl(build_ptab_kernel, dim3((P.Jh + threads - 1) / threads, P.R + 1), dim3(threads),
-                     0, st, P, a_tab, b_tab, sect_fac, ptab));
+                     0, st, P, a_tab, b_tab, sect_fac, ptab, syn));
   SW_LAUNCH_CHECK();
   return kOk;
 }
@@ -1369,7 +1376,178 @@ int launch_ana_tma(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t s
   return kOk;
 }
 
+// ---------------------------------------------------------------------------
+// Synthesis on the FP64 tensor cores (opt-in comparison, SWSDC_SYN_DMMA=1; the
+// north star keeps DMMA only where it beats the vector pipe, and here it does
+// not: config 1 31.3 us vs 29.1 us for syn_kernel, profiles/r02/experiments.md),
+// for batches of >= 8 fields with a plan table: the DFMA kernel is bound by its per-degree coefficient
+// broadcasts (one shared-memory load per 2 latitudes x 2 FMAs), so for wide
+// batches the contraction F[r, j] = sum_s P[r, s, j] c[r, s] runs as DMMA
+// with the product transposed, C^T = c^T P: M = 8 columns (re / im of 4
+// fields), N = 8 latitudes, K = 4 degrees of one parity (even degrees -> E,
+// odd -> O).  A = coefficients (staged per 32-degree chunk in shared memory,
+// shared by the CTA's warps), B = Pbar from the plan's synthesis-order table
+// (reference-rounded, streamed through a per-warp cp.async ring).
+// CTA = one r-pair {p, R - p} of one 16-field group, one warp per 32
+// latitudes; CT column tiles (8 columns each) of 2 x min(B, 16) columns.
+// ---------------------------------------------------------------------------
+constexpr int kSdDepth = 4;           // ring depth in k-steps (1 KB of B per k-step)
+constexpr int kSdCS = 36;             // coefficient tile row stride (doubles)
+
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
+}
+
+template <int CT>
+__global__ void __launch_bounds__(256) syn_dmma_kernel(PlanDev P, SynArgs a, int nf, int ntot) {
+  pdl_wait();
+  pdl_trigger();
+  // field group blockIdx.y: fields [y nf, min((y + 1) nf, ntot))
+  nf = min(nf, ntot - (int)blockIdx.y * nf);
+  extern __shared__ __align__(16) double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nlb = (P.Jh + 31) >> 5;
+  double* cs = smem;                                           // [2][32 degrees][kSdCS]
+  double* ring = smem + 2 * 32 * kSdCS + (size_t)warp * kSdDepth * 128;
+  const double2* src = a.src + (size_t)blockIdx.y * a.src_mstride;
+  double2* eo = a.eo + (size_t)blockIdx.y * a.eo_mstride;
+  const int p = blockIdx.x;
+  const int rows[2] = {p, P.R - p};
+  const int nrow = rows[1] > rows[0] ? 2 : 1;
+  const int lb = warp;                                         // latitude block of this warp
+  const bool lb_ok = lb < nlb;
+  for (int ir = 0; ir < nrow; ++ir) {
+    const int r = rows[ir];
+    const int nst = a.smax - r + 1, nch = (nst + kChunk - 1) / kChunk;
+    // coefficient staging of chunk ci into buffer ci & 1: row d = degree r + 32 ci + d,
+    // columns 2 f + (re, im); zero past the input truncation / the row end
+    auto stage = [&](int ci) {
+      double* dst = cs + (size_t)(ci & 1) * 32 * kSdCS;
+      for (int idx = threadIdx.x; idx < 32 * 8 * CT / 2; idx += blockDim.x) {
+        const int d = idx / (4 * CT), f = idx - d * (4 * CT);
+        const int sdeg = r + ci * kChunk + d;
+        const bool valid = f < nf && r <= a.src_R && sdeg <= a.src_R && sdeg <= a.smax;
+        const double2* gp = src + (size_t)f * a.src_fstride + (size_t)r * (a.src_R + 1) + (valid ? sdeg : r);
+        cp_async16_zfill(dst + d * kSdCS + 2 * f, valid ? gp : src, valid);
+      }
+    };
+    // B fragments of (chunk ci, k-step ks) for this warp's latitude block
+    const double* tab = P.stab + ((size_t)P.ck_off[r] * nlb + lb) * 8 * 128;
+    auto issue = [&](int i) {   // i = ci * 8 + ks
+      if (lb_ok && i < nch * 8) {
+        const double* s0 = tab + (size_t)(i >> 3) * nlb * 8 * 128 + (size_t)(i & 7) * 128;
+        double* d0 = ring + (i % kSdDepth) * 128;
+        cp_async16_ana(d0 + 2 * lane, s0 + 2 * lane);
+        cp_async16_ana(d0 + 64 + 2 * lane, s0 + 64 + 2 * lane);
+      }
+    };
+    double acc[2][CT][4][2];
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+      for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+        for (int lt = 0; lt < 4; ++lt) { acc[pp][ct][lt][0] = 0.0; acc[pp][ct][lt][1] = 0.0; }
+    __syncthreads();                 // the previous row's last tile reads are done
+    stage(0);
+    cp_async_commit();
+#pragma unroll
+    for (int d = 0; d < kSdDepth - 1; ++d) { issue(d); cp_async_commit(); }
+    for (int ci = 0; ci < nch; ++ci) {
+      if (ci + 1 < nch) stage(ci + 1);
+      cp_async_commit();
+      const double* ct0 = cs + (size_t)(ci & 1) * 32 * kSdCS;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int i = ci * 8 + ks;
+        issue(i + kSdDepth - 1);
+        cp_async_commit();
+        // the group of k-step i (and the chunk's coefficients) have landed
+        cp_async_wait<kSdDepth - 1>();
+        if (ks == 0) __syncthreads();   // every thread's coefficient copies of chunk ci
+        else __syncwarp();
+        const int pp = ks >> 2, q = ks & 3;
+        const double* rb = ring + (i % kSdDepth) * 128;
+        double bv[4], av[CT];
+#pragma unroll
+        for (int lt = 0; lt < 4; ++lt) bv[lt] = rb[lt * 32 + lane];
+        const int drow = pp + 2 * (4 * q + t);   // degree row of this lane's A element
+#pragma unroll
+        for (int ct = 0; ct < CT; ++ct) av[ct] = ct0[drow * kSdCS + 8 * ct + g];
+#pragma unroll
+        for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+          for (int lt = 0; lt < 4; ++lt) dmma884(acc[pp][ct][lt], av[ct], bv[lt]);
+        __syncwarp();
+      }
+      __syncthreads();   // the coefficient buffer of chunk ci is refilled at ci + 2
+    }
+    cp_async_wait<0>();
+    // E / O out: lane (g, t) holds column 8 ct + g (field (8 ct + g) / 2, re for even g,
+    // im for odd g) at latitudes 32 lb + 8 lt + 2 t + {0, 1}
+    if (lb_ok) {
+#pragma unroll
+      for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+        for (int lt = 0; lt < 4; ++lt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double E = acc[0][ct][lt][e], O = acc[1][ct][lt][e];
+            const double Ei = __shfl_down_sync(0xffffffffu, E, 4);
+            const double Oi = __shfl_down_sync(0xffffffffu, O, 4);
+            const int f = (8 * ct + g) >> 1;
+            const int jh = 32 * lb + 8 * lt + 2 * t + e;
+            if (!(g & 1) && f < nf && jh < P.Jh) {
+              double2* o = eo + (size_t)f * ((size_t)(P.R + 1) * P.Jh * 2) + ((size_t)r * P.Jh + jh) * 2;
+              o[0] = make_double2(E, Ei);
+              o[1] = make_double2(O, Oi);
+            }
+          }
+    }
+  }
+}
+
+template <int CT>
+int launch_syn_dmma_t(const PlanDev& P, const SynArgs& a, int nf, int ntot, cudaStream_t st) {
+  const int npairs = P.R / 2 + 1;
+  const int nlb = (P.Jh + 31) / 32;
+  const int warps = nlb;
+  const size_t smem = sizeof(double) * (2 * 32 * kSdCS + (size_t)warps * kSdDepth * 128);
+  auto kern = syn_dmma_kernel<CT>;
+  SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
+  StageScope sc("legendre_synthesis", st);
+  SW_CUDA(launch_pdl(kern, dim3(npairs, a.nmembers), dim3(32 * warps), smem, st, P, a, nf, ntot));
+  SW_LAUNCH_CHECK();
+  return kOk;
+}
+
 }  // namespace
+
+// Tensor-core synthesis of nf <= 16 plain fields per member (a.nmembers groups):
+// needs the plan's synthesis table (P.stab) and Jh <= 256 (one warp per 32
+// latitudes in a CTA of <= 8 warps).
+int launch_synthesis_dmma(const PlanDev& P, const SynArgs& a, int nf, cudaStream_t st) {
+  if (!P.stab || nf < 1 || nf > 16 || (P.Jh + 31) / 32 > 8 || a.pairs) {
+    set_error("tensor-core synthesis needs a plan table, <= 16 fields and <= 256 latitude pairs");
+    return kUsage;
+  }
+  // field groups of <= 8 (2 column tiles) per CTA: twice the CTAs of one 16-field group
+  static const int gf = std::max(1, std::min(16, env_int("SWSDC_SYN_DMMA_GF", 8)));
+  const int ng = (nf + gf - 1) / gf, per = (nf + ng - 1) / ng;
+  SynArgs b = a;
+  b.nmembers = ng;
+  b.src_mstride = a.src_fstride * per;
+  b.eo_mstride = (long long)(P.R + 1) * P.Jh * 2 * per;
+  switch ((2 * per + 7) / 8) {
+    case 1: return launch_syn_dmma_t<1>(P, b, per, nf, st);
+    case 2: return launch_syn_dmma_t<2>(P, b, per, nf, st);
+    case 3: return launch_syn_dmma_t<3>(P, b, per, nf, st);
+    default: return launch_syn_dmma_t<4>(P, b, per, nf, st);
+  }
+}
 
 int ana_warps_per_cta() { return kAnaWarps; }
 int ana_chunks_per_cta(int lsplit) { return lsplit >= 3 ? 1 : kAnaWarps / lsplit; }

@@ -55,8 +55,11 @@ int ana_ctas_per_sm(int nv, int lsplit, bool tab);
 bool ana_table_fed(const PlanDev& P, int nt, int mp);
 // Fragment-native Pbar table for the table-fed analysis (see build_ptab in legendre.cu):
 // nck chunks x jh4 4-latitude blocks x 128 doubles; ptab must be zero-initialised.
+// syn = 1: the synthesis-order table (P.stab, see syn_dmma_kernel): per (chunk, 32-latitude
+// block) 8 k-steps x 128 doubles.
 int build_ptab(const PlanDev& P, const double* a_tab, const double* b_tab, const double* sect_fac,
-               double* ptab, cudaStream_t st);
+               double* ptab, cudaStream_t st, int syn = 0);
+int launch_synthesis_dmma(const PlanDev& P, const SynArgs& a, int nf, cudaStream_t st);
 constexpr int kAnaSplits = 4;
 bool ana_uses_tma(int nv);
 bool ana_dfma_enabled();   // SWSDC_ANA_DFMA comparison kernel selected

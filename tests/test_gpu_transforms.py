@@ -171,3 +171,41 @@ def test_long_rings_match_oracle(R, I, J):
     ofe = orhs.eval_fe(x)
     for f in range(3):
         assert rel_err(fe[f], ofe[f]) < TOL
+
+
+def test_round2_kernel_variants_match_reference():
+    """Round-2 alternatives behind knobs (read once per process, so each runs in a
+    subprocess): the opt-in tensor-core synthesis (SWSDC_SYN_DMMA=1, 4/8/16 fields
+    per CTA), the recurrence-only analysis (SWSDC_TABLES=0), the 12-FFT fused grid
+    kernel (SWSDC_SWE_G5=0) and the column-major F_E layout (SWSDC_FE_PM=0) give
+    the reference's synthesis and F_E."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "from conftest import GOLDEN, TEST_PARAMS, rel_err;"
+        "from paper_1805_07923_b200 import spharm, swe;"
+        "g = np.load(GOLDEN + '/transforms.npz'); h = np.load(GOLDEN + '/rhs.npz');"
+        "worst = 0.0\n"
+        "for R, I, J in [(31, 96, 48), (63, 192, 96), (31, 96, 47)]:\n"
+        "    t = f'R{R}_I{I}_J{J}'\n"
+        "    plan = spharm.TransformPlan(spharm.build_gaussian_grid(J, I), R)\n"
+        "    for nb in (3, 8, 15, 20):\n"
+        "        c = np.stack([g[t + '_c']] * nb)\n"
+        "        s = plan.synthesize(c)\n"
+        "        worst = max(worst, max(rel_err(s[k], g[t + '_syn']) for k in range(nb)))\n"
+        "for R, I, J in [(15, 48, 24), (31, 96, 47), (31, 96, 48)]:\n"
+        "    t = f'R{R}_I{I}_J{J}'\n"
+        "    plan = spharm.TransformPlan(spharm.build_gaussian_grid(J, I), R)\n"
+        "    rhs = swe.ShallowWaterRHS(plan, swe.ModelParams(**TEST_PARAMS))\n"
+        "    fe = rhs.eval_f_e(swe.PrognosticState(h[t + '_x'])).numpy()\n"
+        "    worst = max(worst, max(rel_err(fe[f], h[t + '_fe_nl1'][f]) for f in range(3)))\n"
+        "print(worst)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for env in ({"SWSDC_SYN_DMMA": "1"}, {"SWSDC_SYN_DMMA": "1", "SWSDC_SYN_DMMA_GF": "4"},
+                {"SWSDC_SYN_DMMA": "1", "SWSDC_SYN_DMMA_GF": "16"}, {"SWSDC_TABLES": "0"},
+                {"SWSDC_SWE_G5": "0"}, {"SWSDC_FE_PM": "0"}):
+        out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True,
+                             text=True, env={**os.environ, **env}, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        assert float(out.stdout.strip().splitlines()[-1]) < TOL, (env, out.stdout)
