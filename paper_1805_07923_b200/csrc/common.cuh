@@ -45,6 +45,7 @@ void set_error(const std::string& msg);
 // Raise a kernel's dynamic shared-memory limit once per (kernel, device) and
 // size growth instead of on every launch (profile.cu).
 int set_max_dyn_smem(const void* kern, size_t smem);
+int set_smem_carveout_max(const void* kern);
 // Integer tuning knob from the environment, `dflt` when unset; callers cache it
 // in a function-local static so the environment is read once per process.
 int env_int(const char* name, int dflt);

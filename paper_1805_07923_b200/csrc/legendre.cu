@@ -838,11 +838,21 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
   }
   ANA_STAMP(4);
 
+  // only the LSPLIT warps of one chunk meet: the whole CTA for LSPLIT >= 3 (one
+  // chunk per CTA), named barriers 1 / 2 with immediate ids for LSPLIT = 2 -- a
+  // register-valued barrier id would reserve all 16 ids and cap the kernel at 4
+  // CTAs per SM (ncu: "Block Limit Barriers")
+  auto chunk_barrier = [&]() {
+    if constexpr (LSPLIT >= 3) {
+      __syncthreads();
+    } else {
+      if (warp < LSPLIT) asm volatile("bar.sync 1, %0;\n" ::"n"(32 * LSPLIT) : "memory");
+      else asm volatile("bar.sync 2, %0;\n" ::"n"(32 * LSPLIT) : "memory");
+    }
+  };
   if (LSPLIT > 1) {
-    // warps half > 0 hand their partial sums to the half-0 warp of their chunk;
-    // only the LSPLIT warps of one chunk meet (named barrier 1 + chunk)
-    const unsigned bar_id = 1 + warp / LSPLIT, bar_n = 32 * LSPLIT;
-    asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
+    // warps half > 0 hand their partial sums to the half-0 warp of their chunk
+    chunk_barrier();
     double* red = smem + (size_t)warp * ana_warp_doubles<NT, TAB, PM>();
     if (half > 0 && active) {
 #pragma unroll
@@ -856,7 +866,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
             red[(e + 1) * 32 + lane] = acc[p][mt][n][1];
           }
     }
-    asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(bar_n) : "memory");
+    chunk_barrier();
     if (!active) return;
     if (half > 0) return;
     for (int h = 1; h < LSPLIT; ++h) {
@@ -914,7 +924,7 @@ __device__ __forceinline__ void ana_item(const PlanDev& P, const AnaArgs& a, con
 
 // One CTA per work item (grid: items x members).
 template <int NT, int LSPLIT, int MP = 1, bool TAB = false, bool PM = false>
-__global__ void __launch_bounds__(kAnaWarps * 32)
+__global__ void __launch_bounds__(kAnaWarps * 32, 4)
 ana_kernel(PlanDev P, AnaArgs a) {
   pdl_trigger();   // pdl_wait() inside ana_item, after the plan-table loads
   extern __shared__ __align__(16) double smem[];
@@ -1117,6 +1127,7 @@ int launch_ana_pairs_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream
   auto kern = pm ? (tab ? ana_kernel<4, LSPLIT, 2, true, true> : ana_kernel<4, LSPLIT, 2, false, true>)
                  : (tab ? ana_kernel<4, LSPLIT, 2, true> : ana_kernel<4, LSPLIT, 2>);
   SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
+  SW_TRY(set_smem_carveout_max(reinterpret_cast<const void*>(kern)));
   StageScope sc("legendre_analysis", st);
   SW_CUDA(launch_pdl(kern, dim3(dim3(nwork, a.nmembers)), dim3(warps * 32), smem, st, P, a));
   SW_LAUNCH_CHECK();
@@ -1142,6 +1153,7 @@ int launch_ana_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st)
       const size_t smem = sizeof(double) * warps * ana_warp_doubles<NT, false, true>();
       auto kern = ana_kernel<NT, LSPLIT, 1, false, true>;
       SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
+      SW_TRY(set_smem_carveout_max(reinterpret_cast<const void*>(kern)));
       StageScope sc("legendre_analysis", st);
       SW_CUDA(launch_pdl(kern, dim3(dim3(nwork, a.nmembers)), dim3(warps * 32), smem, st, P, a));
       SW_LAUNCH_CHECK();
@@ -1154,6 +1166,7 @@ int launch_ana_t(const PlanDev& P, const AnaArgs& a, int nwork, cudaStream_t st)
   const size_t smem = sizeof(double) * warps * (tab ? ana_warp_doubles<NT, true>() : ana_warp_doubles<NT>());
   auto kern = tab ? ana_kernel<NT, LSPLIT, 1, true> : ana_kernel<NT, LSPLIT>;
   SW_TRY(set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem));
+  SW_TRY(set_smem_carveout_max(reinterpret_cast<const void*>(kern)));
   StageScope sc("legendre_analysis", st);
   SW_CUDA(launch_pdl(kern, dim3(dim3(nwork, a.nmembers)), dim3(warps * 32), smem, st, P, a));
   SW_LAUNCH_CHECK();
@@ -1180,6 +1193,7 @@ int ana_ctas_per_sm_t(bool tab) {
   auto kern = dfma ? ana_dfma_kernel<NT, LSPLIT>
                    : tab ? ana_kernel<NT, LSPLIT, 1, true> : ana_kernel<NT, LSPLIT>;
   if (set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem) != kOk) return 1;
+  if (!dfma && set_smem_carveout_max(reinterpret_cast<const void*>(kern)) != kOk) return 1;
   int n = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, warps * 32, smem) != cudaSuccess) {
     cudaGetLastError();

@@ -51,6 +51,25 @@ int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
+// Prefer the largest shared-memory carveout (228 KB of the 256 KB L1/smem) for a
+// kernel whose occupancy is smem-limited (otherwise the driver may pick 168 KB).
+int set_smem_carveout_max(const void* kern) {
+  static const int knob = env_int("SWSDC_CARVEOUT", 1);
+  if (!knob) return kOk;
+  static std::mutex mu;
+  static std::map<const void*, bool> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[kern]) return kOk;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             (int)cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaFuncSetAttribute(carveout): ") + cudaGetErrorString(e));
+    return kCuda;
+  }
+  done[kern] = true;
+  return kOk;
+}
+
 int set_max_dyn_smem(const void* kern, size_t smem) {
   if (smem <= 48 * 1024) return kOk;
   static std::mutex mu;
