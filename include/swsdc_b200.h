@@ -119,6 +119,15 @@ int swsdc_spec_combine_multi(int nout, const int* nterms, const double* const* x
                              const int* ext, void* stream);
 /* dst = src over n doubles and *bad = (any value non-finite): the stepper's per-step state
  * copy and finiteness check (harness.py:257) in one pass; *bad is cleared first. */
+/* m-sharding exchange packing (distributed.py, exchange_eo / exchange_x): for the array
+ * arr[outer][rows][cols][inner] (doubles) and nblocks (<= 64) blocks b -- rows row0[b] +
+ * k row_step[b] (k < nrows[b]), columns [col0[b], col1[b]) -- gather them into the contiguous
+ * buffer buf, block after block as [b][outer][k][col][inner] (scatter = 0), or scatter buf
+ * back into arr (scatter = 1).  One launch instead of one strided copy per peer. */
+int swsdc_exchange_blocks(double* arr, long long outer, long long rows, long long cols,
+                          long long inner, int nblocks, const int* row0, const int* row_step,
+                          const int* nrows, const int* col0, const int* col1, double* buf,
+                          int scatter, void* stream);
 int swsdc_copy_finite(const double* src, double* dst, long long n, int* bad, void* stream);
 /* One SDC node update (sdc.py:196-206): b = sum_k w[k] x[k] (states at truncation R),
  * theta = solve_implicit(b, beta) (implicit.py:31-49), f_i = eval_f_i(theta)

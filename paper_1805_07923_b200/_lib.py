@@ -58,6 +58,7 @@ _SIGNATURES = {
     "swsdc_upload_coeffs": ([_P, _I, _LL, _P, _P], _I),
     "swsdc_spec_combine_multi": ([_I, _P, _P, _P, _P, _I, _LL, _P, _P, _P], _I),
     "swsdc_copy_finite": ([_P, _P, _LL, _P, _P], _I),
+    "swsdc_exchange_blocks": ([_P, _LL, _LL, _LL, _LL, _I, _P, _P, _P, _P, _P, _P, _I, _P], _I),
     "swsdc_download_coeffs": ([_P, _I, _LL, _P, _I, _P], _I),
     "swsdc_spec_combine": ([_I, ctypes.POINTER(_P), ctypes.POINTER(_D), ctypes.POINTER(_I), _I, _LL,
                             _P, _P], _I),

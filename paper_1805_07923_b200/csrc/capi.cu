@@ -924,6 +924,37 @@ int swsdc_spec_combine(int n, const double* const* x, const double* w, const int
   return launch_spec_combine(a, nmat, S(stream));
 }
 
+int swsdc_exchange_blocks(double* arr, long long outer, long long rows, long long cols, long long inner,
+                          int nblocks, const int* row0, const int* row_step, const int* nrows,
+                          const int* col0, const int* col1, double* buf, int scatter,
+                          void* stream) {
+  if (nblocks < 0 || nblocks > kMaxExBlocks || outer < 0 || rows < 0 || cols < 0 || inner < 1) {
+    set_error("exchange_blocks: bad dimensions or more than 64 blocks");
+    return kUsage;
+  }
+  ExchangeBlocks e{};
+  e.rows = rows;
+  e.cols = cols;
+  e.C = inner;
+  e.nb = nblocks;
+  e.off[0] = 0;
+  for (int b = 0; b < nblocks; ++b) {
+    const long long last = row0[b] + (long long)(nrows[b] - 1) * row_step[b];
+    if (nrows[b] < 0 || col0[b] < 0 || col1[b] < col0[b] || col1[b] > cols || row0[b] < 0 ||
+        (nrows[b] > 0 && (last >= rows || last < 0))) {
+      set_error("exchange_blocks: block outside the array");
+      return kUsage;
+    }
+    e.row0[b] = row0[b];
+    e.row_step[b] = row_step[b];
+    e.nrows[b] = nrows[b];
+    e.col0[b] = col0[b];
+    e.col1[b] = col1[b];
+    e.off[b + 1] = e.off[b] + outer * nrows[b] * (long long)(col1[b] - col0[b]) * inner;
+  }
+  return launch_exchange_blocks(e, arr, buf, scatter != 0, S(stream));
+}
+
 int swsdc_copy_finite(const double* src, double* dst, long long n, int* bad, void* stream) {
   if (n < 0 || !bad) { set_error("bad copy_finite arguments"); return kUsage; }
   return launch_copy_finite(src, dst, n, bad, S(stream));

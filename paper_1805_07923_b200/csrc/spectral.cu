@@ -540,6 +540,35 @@ __global__ void zero_lower_kernel(double2* out, int R, long long nmat) {
 // dst = src over n doubles; *bad = 1 if any value is not finite (*bad is
 // cleared by the caller first): the graph stepper's state copy and per-step
 // finiteness check (harness.py:257) in one pass.
+// m-sharding exchange packing (distributed.py): blocks b of a [A][rows][cols][C]
+// double array -- rows row0_b + k row_step_b (k < nrows_b), columns
+// [col0_b, col1_b) -- gathered into (scatter = 0) or scattered from
+// (scatter = 1) one contiguous buffer, block after block in order
+// [b][A][k][col][C].  One launch replaces P strided copies per exchange.
+__global__ void __launch_bounds__(256) exchange_blocks_kernel(ExchangeBlocks e, double* arr,
+                                                               double* buf, int scatter) {
+  pdl_wait();
+  pdl_trigger();
+  const long long total = e.off[e.nb];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int b = 0;
+    while (i >= e.off[b + 1]) ++b;
+    long long rem = i - e.off[b];
+    const int ncol = e.col1[b] - e.col0[b];
+    const int c = (int)(rem % e.C);
+    rem /= e.C;
+    const int col = e.col0[b] + (int)(rem % ncol);
+    rem /= ncol;
+    const int k = (int)(rem % e.nrows[b]);
+    const long long a = rem / e.nrows[b];
+    const long long row = e.row0[b] + (long long)k * e.row_step[b];
+    double* x = arr + ((a * e.rows + row) * e.cols + col) * e.C + c;
+    if (scatter) *x = buf[i];
+    else buf[i] = *x;
+  }
+}
+
 __global__ void __launch_bounds__(256) copy_finite_kernel(const double* __restrict__ src,
                                                           double* __restrict__ dst, long long n,
                                                           int* bad) {
@@ -553,6 +582,17 @@ __global__ void __launch_bounds__(256) copy_finite_kernel(const double* __restri
     ok = ok && isfinite(v);
   }
   if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicExch(bad, 1);
+}
+
+int launch_exchange_blocks(const ExchangeBlocks& e, double* arr, double* buf, int scatter,
+                           cudaStream_t st) {
+  const long long n = e.off[e.nb];
+  if (n == 0) return kOk;
+  StageScope sc("exchange_pack", st);
+  SW_CUDA(launch_pdl(exchange_blocks_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, e, arr, buf,
+                     scatter));
+  SW_LAUNCH_CHECK();
+  return kOk;
 }
 
 int launch_copy_finite(const double* src, double* dst, long long n, int* bad, cudaStream_t st) {

@@ -69,6 +69,16 @@ int launch_upload_triangle(const double2* host, double2* out, int R, long long n
                            cudaStream_t st);
 int launch_download_triangle(const double2* dev, double2* host, int R, long long nmat,
                              int write_lower, cudaStream_t st);
+constexpr int kMaxExBlocks = 64;
+struct ExchangeBlocks {
+  long long rows, cols, C;            // array dims after the outer one: [A][rows][cols][C]
+  int nb;
+  int row0[kMaxExBlocks], row_step[kMaxExBlocks], nrows[kMaxExBlocks];
+  int col0[kMaxExBlocks], col1[kMaxExBlocks];
+  long long off[kMaxExBlocks + 1];    // doubles before block b in the buffer
+};
+int launch_exchange_blocks(const ExchangeBlocks& e, double* arr, double* buf, int scatter,
+                           cudaStream_t st);
 int launch_copy_finite(const double* src, double* dst, long long n, int* bad, cudaStream_t st);
 int launch_zero_lower(double2* out, int R, long long nmat, cudaStream_t st);
 int launch_resize(const double2* in, int rin, double2* out, int rout, long long nmat,

@@ -96,6 +96,21 @@ class TorchExchanger:
             r.wait()
         return [t.to(dev) for t in recvs]
 
+    def all_to_all_flat(self, sbuf: torch.Tensor, ssizes: list[int], rbuf: torch.Tensor,
+                        rsizes: list[int]) -> torch.Tensor:
+        """One all-to-all of contiguous per-peer segments (all_to_all_single with
+        split sizes: one NCCL collective); gloo stages device buffers through host."""
+        if self.native:
+            self.dist.all_to_all_single(rbuf, sbuf, output_split_sizes=list(rsizes),
+                                        input_split_sizes=list(ssizes), group=self.group)
+            return rbuf
+        hs = sbuf.detach().to("cpu")
+        hr = torch.empty(rbuf.shape, dtype=rbuf.dtype)
+        self.dist.all_to_all_single(hr, hs, output_split_sizes=list(rsizes),
+                                    input_split_sizes=list(ssizes), group=self.group)
+        rbuf.copy_(hr)
+        return rbuf
+
     def all_gather(self, mine: torch.Tensor) -> list[torch.Tensor]:
         """Every rank's `mine` (equal shapes), in rank order."""
         if self.native:
@@ -138,6 +153,12 @@ class _LocalRank:
     def all_gather(self, mine):
         return self.all_to_all([mine] * self.P, [tuple(mine.shape)] * self.P)
 
+    def all_to_all_flat(self, sbuf, ssizes, rbuf, rsizes):
+        sends = list(torch.split(sbuf, list(ssizes)))
+        got = self.all_to_all(sends, [(n,) for n in rsizes])
+        torch.cat(got, out=rbuf)
+        return rbuf
+
     def all_reduce_max(self, t):
         got = self.all_to_all([t] * self.P, [tuple(t.shape)] * self.P)
         return torch.stack(got).amax(dim=0)
@@ -159,10 +180,46 @@ class _LocalRank:
 # exchange packing (pure torch: unit-tested on CPU with gloo)
 # ----------------------------------------------------------------------------
 
+def _blocks(arr: torch.Tensor, outer: int, rows: int, cols: int, inner: int, blocks,
+            buf: torch.Tensor | None, scatter: bool) -> torch.Tensor:
+    """swsdc_exchange_blocks: gather (scatter=False) blocks (row0, row_step, nrows,
+    col0, col1) of arr[outer][rows][cols][inner] into one contiguous buffer, or
+    scatter the buffer back -- one library launch."""
+    nb = len(blocks)
+    arrs = [(ctypes.c_int * nb)(*[b[i] for b in blocks]) for i in range(5)]
+    if buf is None:
+        n = sum(outer * b[2] * (b[4] - b[3]) * inner for b in blocks)
+        buf = torch.empty(n, dtype=torch.float64, device=arr.device)
+    _lib.check(_lib.load().swsdc_exchange_blocks(_ptr(arr), outer, rows, cols, inner, nb, *arrs,
+                                                 _ptr(buf), 1 if scatter else 0,
+                                                 _stream_ptr(arr.device)))
+    return buf
+
+
+def _seg_sizes(outer, inner, blocks):
+    return [outer * b[2] * (b[4] - b[3]) * inner for b in blocks]
+
+
 def exchange_eo(ex, spec: ShardSpec, eo: torch.Tensor, R: int, Jh: int, jh4: int) -> torch.Tensor:
     """eo [m, 5, R+1, Jh, 4] with valid own rows -> same shape with ALL rows valid
-    for this rank's latitude pairs."""
+    for this rank's latitude pairs.  Device tensors: one pack launch, one flat
+    all-to-all, one unpack launch (swsdc_exchange_blocks); host tensors (the gloo
+    CPU tests) take the equivalent torch slicing below."""
     P = spec.P
+    if eo.is_cuda and hasattr(ex, "all_to_all_flat"):
+        m, f = eo.shape[0], eo.shape[1]
+        arr = eo.contiguous()
+        nmine = len(range(spec.rank, R + 1, P))
+        sblocks = [(spec.rank, P, nmine, *spec.lat_bounds(q, jh4, Jh)) for q in range(P)]
+        j0, j1 = spec.lat_bounds(spec.rank, jh4, Jh)
+        rblocks = [(p, P, len(range(p, R + 1, P)), j0, j1) for p in range(P)]
+        sbuf = _blocks(arr, m * f, R + 1, Jh, 4, sblocks, None, False)
+        rs = _seg_sizes(m * f, 4, rblocks)
+        rbuf = torch.empty(sum(rs), dtype=torch.float64, device=eo.device)
+        ex.all_to_all_flat(sbuf, _seg_sizes(m * f, 4, sblocks), rbuf, rs)
+        out = torch.empty_like(arr)
+        _blocks(out, m * f, R + 1, Jh, 4, rblocks, rbuf, True)
+        return out
     rows = spec.rows(R)
     sends, shapes = [], []
     m = eo.shape[0]
@@ -183,8 +240,22 @@ def exchange_eo(ex, spec: ShardSpec, eo: torch.Tensor, R: int, Jh: int, jh4: int
 def exchange_x(ex, spec: ShardSpec, x: torch.Tensor, R: int, jh4: int) -> torch.Tensor:
     """x [m, G, R+1, jh4, F] (fragment-native analysis input, F = 2*nc*4) valid for
     all rows on this rank's latitude blocks -> same shape valid for own rows on
-    ALL latitude blocks."""
+    ALL latitude blocks (device tensors: library pack / flat all-to-all / unpack)."""
     P = spec.P
+    if x.is_cuda and hasattr(ex, "all_to_all_flat"):
+        m, G, F = x.shape[0], x.shape[1], x.shape[-1]
+        arr = x.contiguous()
+        b0, b1 = spec.block_bounds(spec.rank, jh4)
+        sblocks = [(p, P, len(range(p, R + 1, P)), b0, b1) for p in range(P)]
+        nmine = len(range(spec.rank, R + 1, P))
+        rblocks = [(spec.rank, P, nmine, *spec.block_bounds(q, jh4)) for q in range(P)]
+        sbuf = _blocks(arr, m * G, R + 1, jh4, F, sblocks, None, False)
+        rs = _seg_sizes(m * G, F, rblocks)
+        rbuf = torch.empty(sum(rs), dtype=torch.float64, device=x.device)
+        ex.all_to_all_flat(sbuf, _seg_sizes(m * G, F, sblocks), rbuf, rs)
+        out = torch.empty_like(arr)
+        _blocks(out, m * G, R + 1, jh4, F, rblocks, rbuf, True)
+        return out
     sends, shapes = [], []
     b0, b1 = spec.block_bounds(spec.rank, jh4)
     for p in range(P):

@@ -58,6 +58,16 @@ def _worker(rank, world, port, R, Jh, fails):
         mine[..., rank:R + 1:world, :] = st[..., rank:R + 1:world, :]
         got = gather_state(ex, spec, mine)
         assert torch.equal(got, st), "gather_state"
+        # --- flat all-to-all (the device path's single collective with split sizes)
+        ssizes = [q + 1 + rank for q in range(world)]        # to q: q+1+rank values
+        rsizes = [rank + 1 + p for p in range(world)]        # from p: rank+1+p values
+        sbuf = torch.cat([torch.full((n,), 100.0 * rank + q, dtype=torch.float64)
+                          for q, n in enumerate(ssizes)])
+        rbuf = torch.empty(sum(rsizes), dtype=torch.float64)
+        ex.all_to_all_flat(sbuf, ssizes, rbuf, rsizes)
+        want = torch.cat([torch.full((n,), 100.0 * p + rank, dtype=torch.float64)
+                          for p, n in enumerate(rsizes)])
+        assert torch.equal(rbuf, want), "flat all-to-all"
         # --- per-step finiteness flag: a NaN in one rank's own rows reaches every rank
         from paper_1805_07923_b200.distributed import owned_nonfinite
         clean = owned_nonfinite(spec, st)

@@ -41,3 +41,21 @@ def test_public_transforms_refuse_row_filter():
                 call()
     # outside the filter the same calls work
     assert np.isfinite(plan.analyze(g).cpu().numpy()).all()
+
+
+def test_exchange_blocks_gather_scatter_roundtrip():
+    """swsdc_exchange_blocks (the m-sharding pack / unpack launch) equals torch
+    slicing of the same blocks, and scatter inverts gather."""
+    from paper_1805_07923_b200 import distributed as D
+    g = torch.Generator(device="cuda").manual_seed(5)
+    arr = torch.randn((6, 13, 11, 4), dtype=torch.float64, device="cuda", generator=g)
+    blocks = [(0, 3, 5, 0, 4), (1, 3, 4, 4, 9), (2, 3, 4, 9, 11), (5, 1, 3, 2, 7)]
+    buf = D._blocks(arr, 6, 13, 11, 4, blocks, None, False)
+    want = torch.cat([arr[:, r0:r0 + (n - 1) * st + 1:st, c0:c1, :].reshape(-1)
+                      for r0, st, n, c0, c1 in blocks])
+    assert torch.equal(buf, want)
+    out = torch.full_like(arr, float("nan"))
+    D._blocks(out, 6, 13, 11, 4, blocks, buf, True)
+    for r0, st, n, c0, c1 in blocks:
+        sl = (slice(None), slice(r0, r0 + (n - 1) * st + 1, st), slice(c0, c1))
+        assert torch.equal(out[sl], arr[sl])
