@@ -278,6 +278,12 @@ int pick_ana_split(int nch, int nmembers, int nv, int Jh, bool tab) {
   // 18.33 ms per config-3 step); small problems keep the wave-fitting choice.
   const long long slots1 = (long long)sms * ana_ctas_per_sm(nv, 1, tab) * ana_chunks_per_cta(1);
   const double item_cost = (long long)nch * nmembers >= 2 * slots1 ? 1.0 : 0.0;
+  // Small problems (about one wave unsplit): three latitude splits measured best
+  // once the kernel runs 5 CTAs/SM (immediate barriers, max carveout): config 1
+  // analysis 28.1 us vs 29.2 (two splits, the wave-fitting choice), config 2 step
+  // 1.733 vs 1.764 ms; fewer latitude blocks than three cap it
+  static const int small3 = env_int("SWSDC_ANA_SMALL3", 1);
+  if (small3 && item_cost == 0.0 && nblk >= 3) return 3;
   int best = 1;
   double best_eff = -1.0;
   for (int ls = 1; ls <= kAnaSplits; ++ls) {
