@@ -1116,46 +1116,50 @@ __global__ void __launch_bounds__(256, 1) swe_prod_kernel(PlanDev P, const doubl
     Fn = d2(E.x + O.x, r == 0 ? 0.0 : E.y + O.y);
     Fs = d2(E.x - O.x, r == 0 ? 0.0 : E.y - O.y);
   };
-  // linear only (include_nonlinear=False): one pass of (A1, A2) -> v0, v1
-  for (int pass = NONLIN ? 0 : 4; pass < (NONLIN ? 3 : 5); ++pass) {
-    const int nr = (pass == 2) ? 1 : 2;
+  // Passes over the grids (each ends with the forward FFTs of its rings and the
+  // analysis vectors they complete): nonlinear -- pass 0: ZU, ZV, KE (3 rings)
+  // -> v1, v6, v2, v5, v3; pass 1: PU, PV -> v0, v4 (U and V are read twice, not
+  // three times); linear only (include_nonlinear=False): pass 4: A1, A2 -> v0, v1.
+  for (int pass = NONLIN ? 0 : 4; pass < (NONLIN ? 2 : 5); ++pass) {
+    const int nr = (pass == 0) ? 3 : 2;
+#pragma unroll 4
     for (int il = threadIdx.x; il < I; il += blockDim.x) {
       const double2 U = gv(0, il), V = gv(1, il);
-      double2 a, b = d2(0.0, 0.0);
-      if (pass == 0) {          // ZU = zeta U ; ZV = zeta V
+      double2 a, b, c = d2(0.0, 0.0);
+      if (pass == 0) {          // ZU = zeta U ; ZV = zeta V ; KE = (U^2 + V^2) / (2 (1 - mu^2))
         const double2 Z = gv(2, il);
         a = d2(Z.x * U.x, Z.y * U.y);
         b = d2(Z.x * V.x, Z.y * V.y);
+        c = d2(0.5 * (U.x * U.x + V.x * V.x) * ic2, 0.5 * (U.y * U.y + V.y * V.y) * ic2);
       } else if (pass == 1) {   // PU = phi U ; PV = phi V
         const double2 Ph = gv(4, il);
         a = d2(Ph.x * U.x, Ph.y * U.y);
         b = d2(Ph.x * V.x, Ph.y * V.y);
-      } else if (pass == 4) {   // linear: A1, A2
+      } else {                  // linear: A1, A2
         const double2 D = gv(3, il), Z = gv(2, il);
         a = d2(-fn * D.x - c2o * V.x, fn * D.y - c2o * V.y);
         b = d2(fn * Z.x - c2o * U.x, -fn * Z.y - c2o * U.y);
-      } else {                  // KE = (U^2 + V^2) / (2 (1 - mu^2))
-        a = d2(0.5 * (U.x * U.x + V.x * V.x) * ic2, 0.5 * (U.y * U.y + V.y * V.y) * ic2);
       }
       const int p = K15 > 0 ? swfft::pad_idx(il) : P.rev[il];
       rings[p] = a;
-      if (nr == 2) rings[RS + p] = b;
+      rings[RS + p] = b;
+      if (nr == 3) rings[2 * RS + p] = c;
     }
     __syncthreads();
     if constexpr (K15 > 0) {
-      swfft::ring_fft15<K15, false>(rings, P.tw);
-      if (nr == 2) swfft::ring_fft15<K15, false>(rings + RS, P.tw);
+      for (int q = 0; q < nr; ++q) swfft::ring_fft15<K15, false>(rings + (size_t)q * RS, P.tw);
     } else {
       fft_forward<BIGP>(rings, nr, P);
     }
     for (int r = threadIdx.x; r <= P.R; r += blockDim.x) {
-      double2 An, As, Bn = d2(0.0, 0.0), Bs = Bn;
+      double2 An, As, Bn, Bs;
       get_pair(rings, P, r, An, As);
-      if (nr == 2) get_pair(rings + RS, P, r, Bn, Bs);
+      get_pair(rings + RS, P, r, Bn, Bs);
       const double rwa = r * wc * ia, wa = wc * ia;
       if (pass == 0) {
         // swe.py:262,265 in Fourier space (f = fn north, -fn south)
-        double2 Un, Us, Vn, Vs, Zn, Zs, Dn, Ds;
+        double2 Un, Us, Vn, Vs, Zn, Zs, Dn, Ds, Kn, Ks;
+        get_pair(rings + 2 * RS, P, r, Kn, Ks);
         coef(0, r, Un, Us);
         coef(1, r, Vn, Vs);
         coef(2, r, Zn, Zs);
@@ -1170,14 +1174,13 @@ __global__ void __launch_bounds__(256, 1) swe_prod_kernel(PlanDev P, const doubl
         put_x(xm, xl, 2, r, jh, cadd2(cscale(A2n, w), ir_scale(Bn, rwa)),
               cadd2(cscale(A2s, w), ir_scale(Bs, rwa)), eq);
         put_x(xm, xl, 5, r, jh, cscale(Bn, wa), cscale(Bs, wa), eq);
+        put_x(xm, xl, 3, r, jh, cscale(Kn, w), cscale(Ks, w), eq);
       } else if (pass == 1) {
         put_x(xm, xl, 0, r, jh, ir_scale(An, -rwa), ir_scale(As, -rwa), eq);
         put_x(xm, xl, 4, r, jh, cscale(Bn, wa), cscale(Bs, wa), eq);
-      } else if (pass == 4) {
+      } else {
         put_x(xm, xl, 0, r, jh, cscale(An, w), cscale(As, w), eq);
         put_x(xm, xl, 1, r, jh, cscale(Bn, w), cscale(Bs, w), eq);
-      } else {
-        put_x(xm, xl, 3, r, jh, cscale(An, w), cscale(As, w), eq);
       }
     }
     __syncthreads();
@@ -1412,8 +1415,9 @@ int swe_prod_launch_k(const PlanDev& P, const double* grids, long long gfield, l
                       const double2* eo, long long eo_fstride, double* x, const XLayout& xl,
                       int nmembers, double omega, double radius, int jh_begin, int jh_end,
                       cudaStream_t st) {
-  // grids in the ring layout (f2g_kernel<., true>): gfield / gmember in double2
-  const size_t smem = sizeof(double2) * 2 * P.ring_stride;
+  // grids in the ring layout (f2g_kernel<., true>): gfield / gmember in double2;
+  // 3 rings for the nonlinear first pass (ZU, ZV, KE)
+  const size_t smem = sizeof(double2) * (NONLIN ? 3 : 2) * P.ring_stride;
   SW_TRY(set_smem((const void*)swe_prod_kernel<NONLIN, BIGP, true, K15>, smem));
   dim3 gridDim(jh_end - jh_begin, nmembers);
   if (gridDim.x == 0) return kOk;
