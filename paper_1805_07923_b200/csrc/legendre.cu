@@ -269,6 +269,16 @@ __device__ __forceinline__ void stage_chunk(const ChunkRegs<B, MODE>& c, double2
       s0 = -radius * ilap[s];
       sp = -radius * ilap[s + 1];
       sm = s >= 1 ? -radius * ilap[s - 1] : 0.0;
+    } else if (s >= 2) {
+      // one division for the three scales: q = (s-1) s (s+1) (s+2) is exact in
+      // fp64 (s <= ~1300), then -a / (s (s+1)) = -a (s-1)(s+2) / q etc. (each one
+      // product more than the direct quotient: <= 1 ulp); three divisions were
+      // ~20% of this kernel's stall samples at T1279 (profiles/r02)
+      const double q = (double)(s - 1) * (double)s * (s + 1.0) * (s + 2.0);
+      const double inv = -radius / q;
+      s0 = ((s - 1.0) * (s + 2.0)) * inv;
+      sp = ((s - 1.0) * (double)s) * inv;
+      sm = ((s + 1.0) * (s + 2.0)) * inv;
     } else {
       s0 = inv_lap_a(s, radius);
       sp = inv_lap_a(s + 1, radius);
