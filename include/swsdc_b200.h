@@ -151,6 +151,15 @@ int swsdc_laplacian(const double* in, double* out, int truncation, long long nma
 int swsdc_upload_coeffs(const double* host, int truncation, long long nmat, double* out,
                         void* stream);
 
+/* Host-only half of the packed upload (SWSDC_UPLOAD_MODE=2): the s >= r triangles of
+ * `nmat` dense (R+1)^2 host matrices, row after row, into `packed`
+ * (nmat (R+1)(R+2)/2 complex values), by the library's pool of packing threads; returns
+ * when done.  swsdc_upload_coeffs in that mode runs this asynchronously into a
+ * page-locked staging buffer, gates the stream on it with a stream memory operation,
+ * moves the buffer with one contiguous copy-engine transfer (the only kind that runs
+ * PCIe full duplex next to a download) and expands it on the device.  No device needed. */
+int swsdc_pack_triangles(const double* dense, int truncation, long long nmat, double* packed);
+
 /* Download of `nmat` dense (R+1)^2 spectral matrices from device `dev` into page-locked
  * host memory by zero-copy stores.  write_lower = 1 writes the full dense matrices (the
  * reference's analyze result, spharm.py:254-256); write_lower = 0 guarantees only the s >= r

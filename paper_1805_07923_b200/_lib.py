@@ -56,6 +56,7 @@ _SIGNATURES = {
     "swsdc_resize": ([_P, _I, _P, _I, _LL, _P], _I),
     "swsdc_laplacian": ([_P, _P, _I, _LL, _D, _I, _P], _I),
     "swsdc_upload_coeffs": ([_P, _I, _LL, _P, _P], _I),
+    "swsdc_pack_triangles": ([_P, _I, _LL, _P], _I),
     "swsdc_spec_combine_multi": ([_I, _P, _P, _P, _P, _I, _LL, _P, _P, _P], _I),
     "swsdc_copy_finite": ([_P, _P, _LL, _P, _P], _I),
     "swsdc_exchange_blocks": ([_P, _LL, _LL, _LL, _LL, _I, _P, _P, _P, _P, _P, _P, _I, _P], _I),

@@ -1076,6 +1076,10 @@ static int upload_mode() {
   static const int m = env_int("SWSDC_UPLOAD_MODE", 0);
   return m;
 }
+static int packed_upload_min_bytes() {
+  static const int m = env_int("SWSDC_PACK_MIN_BYTES", 1 << 20);
+  return m;
+}
 static int download_mode() {
   static const int m = env_int("SWSDC_DOWNLOAD_MODE", 1);
   return m;
@@ -1090,12 +1094,32 @@ int swsdc_upload_coeffs(const double* host, int r, long long nmat, double* out, 
     set_error("swsdc_upload_coeffs: source is not page-locked host memory");
     return kUsage;
   }
-  if (upload_mode() == 0)
+  if (upload_mode() == 2) {
+    // packed upload (hostpack.cu) for transfers worth a copy-engine launch; not
+    // capturable (stream memory operation), so a capturing stream takes the kernel
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(S(stream), &cap);
+    const size_t bytes = sizeof(double2) * (size_t)nmat * (r + 1) * (r + 2) / 2;
+    if (cap == cudaStreamCaptureStatusNone && bytes >= (size_t)packed_upload_min_bytes() &&
+        packed_upload_available())
+      return launch_upload_packed(reinterpret_cast<const double2*>(host),
+                                  reinterpret_cast<double2*>(out), r, nmat, S(stream));
+  }
+  if (upload_mode() != 1)
     return launch_upload_triangle(reinterpret_cast<const double2*>(dptr),
                                   reinterpret_cast<double2*>(out), r, nmat, S(stream));
   SW_TRY(stair_copy(reinterpret_cast<const double2*>(host), reinterpret_cast<double2*>(out), r, nmat,
                     cudaMemcpyHostToDevice, S(stream)));
   return launch_zero_lower(reinterpret_cast<double2*>(out), r, nmat, S(stream));
+}
+
+int swsdc_pack_triangles(const double* dense, int r, long long nmat, double* packed) {
+  if (r < 0 || nmat < 0 || (nmat > 0 && (!dense || !packed))) {
+    set_error("bad pack arguments");
+    return kUsage;
+  }
+  return pack_triangles_host(reinterpret_cast<const double2*>(dense), r, nmat,
+                             reinterpret_cast<double2*>(packed));
 }
 
 int swsdc_download_coeffs(const double* dev, int r, long long nmat, double* host, int write_lower,

@@ -114,8 +114,26 @@ __host__ __device__ constexpr bool reg_fft_k_ok(int K) {
          K == 12 || K == 16 || K == 20 || K == 24;
 }
 
-// Per-lane twiddles of the cross-lane stages h = 16, 8, 4: W_{2h}^(l mod h)
-// on the upper lane of each pair, 1 on the lower one.
+// Cross-lane stages come in two forms.  Odd K: every lane exchanges all K slots with
+// its partner and computes one output of each butterfly (own + partner on the lower
+// lane, (partner - own) * twiddle on the upper one).  Even K (half exchange): a lane
+// pair splits the K butterflies -- the lower lane sends its upper register half
+// (slots >= K/2) and receives the partner's lower half, the upper lane the reverse
+// -- so each lane holds both inputs of K/2 butterflies and computes both outputs:
+// half the shuffles (2 K instead of 4 K 32-bit shuffles per stage) and no multiply
+// by 1 on the lower lanes.  Sums go to slot u, differences to slot u + K/2, which
+// swaps the lane bit with the register-half bit; see ring_out_index for where the
+// spectrum ends up.
+#ifndef SWSDC_FFT_HX
+#define SWSDC_FFT_HX 1   // build with -DSWSDC_FFT_HX=0 for the full-exchange stages (same-box A/B)
+#endif
+template <int K>
+__host__ __device__ constexpr bool half_exchange() { return SWSDC_FFT_HX != 0 && K % 2 == 0; }
+
+// Per-lane twiddles of the cross-lane stages h = 16, 8, 4: W_{2h}^(l mod h).
+// Odd K: on the upper lane of each pair, 1 on the lower one.  Half exchange: on
+// both lanes (they share l mod h), negated on the upper lane whose difference is
+// formed as own - partner.
 // tws: stride of tw relative to an N-point table (a sub-transform of a longer
 // ring reads the longer ring's table: W_N^e = tw[e * tws]).
 template <int K, bool INV>
@@ -125,7 +143,12 @@ __device__ __forceinline__ void cross_twiddles(double2 (&wst)[3], const double2*
   for (int st = 0; st < 3; ++st) {
     const int h = 16 >> st;
     const int j = lane & (h - 1);
-    wst[st] = (lane & h) ? tw_at(tw, j * (16 / h) * K * tws, INV) : mk2(1.0, 0.0);
+    if constexpr (half_exchange<K>()) {
+      const double2 w = tw_at(tw, j * (16 / h) * K * tws, INV);
+      wst[st] = (lane & h) ? mk2(-w.x, -w.y) : w;
+    } else {
+      wst[st] = (lane & h) ? tw_at(tw, j * (16 / h) * K * tws, INV) : mk2(1.0, 0.0);
+    }
   }
 }
 
@@ -152,29 +175,63 @@ __device__ __forceinline__ void ring_fft(double2 (&v)[K], const double2* tw, int
       }
     v[m1] = cmul(v[m1], w);
   }
+  if constexpr (half_exchange<K>()) {
+    constexpr int H = K / 2;
 #pragma unroll
-  for (int st = 0; st < 5; ++st) {
-    const int h = 16 >> st;
-    const bool up = (lane & h) != 0;
-    const double sg = up ? -1.0 : 1.0;
-    const bool rot = (st == 3) && up && (lane & 1);   // h = 2: W_4^1 on odd upper lanes
+    for (int st = 0; st < 5; ++st) {
+      const int h = 16 >> st;
+      const bool up = (lane & h) != 0;
+      const double sg = up ? -1.0 : 1.0;
+      const bool rot = (st == 3) && (lane & 1);   // h = 2: W_4^1 on odd lanes
 #pragma unroll
-    for (int q = 0; q < K; ++q) {
-      double2 p;
-      p.x = __shfl_xor_sync(kFull, v[q].x, h);
-      p.y = __shfl_xor_sync(kFull, v[q].y, h);
-      // lower lane: own + partner; upper lane: (partner - own) * twiddle
-      double2 d = mk2(fma(sg, v[q].x, p.x), fma(sg, v[q].y, p.y));
-      if (st < 3) {
-        d = cmul(d, wst[st]);
-      } else if (st == 3) {
-        const double2 r = rot_mi(d, INV);
-        d = rot ? r : d;
+      for (int u = 0; u < H; ++u) {
+        const double2 kept = up ? v[u + H] : v[u];
+        const double2 send = up ? v[u] : v[u + H];
+        double2 p;
+        p.x = __shfl_xor_sync(kFull, send.x, h);
+        p.y = __shfl_xor_sync(kFull, send.y, h);
+        v[u] = mk2(kept.x + p.x, kept.y + p.y);
+        double2 d = mk2(kept.x - p.x, kept.y - p.y);   // upper lane: -(a - b)
+        if (st < 3) {
+          d = cmul(d, wst[st]);
+        } else {
+          d = mk2(sg * d.x, sg * d.y);
+          if (st == 3) {
+            const double2 r = rot_mi(d, INV);
+            d = rot ? r : d;
+          }
+        }
+        v[u + H] = d;
       }
-      v[q] = d;
+    }
+  } else {
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+      const int h = 16 >> st;
+      const bool up = (lane & h) != 0;
+      const double sg = up ? -1.0 : 1.0;
+      const bool rot = (st == 3) && up && (lane & 1);   // h = 2: W_4^1 on odd upper lanes
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        double2 p;
+        p.x = __shfl_xor_sync(kFull, v[q].x, h);
+        p.y = __shfl_xor_sync(kFull, v[q].y, h);
+        // lower lane: own + partner; upper lane: (partner - own) * twiddle
+        double2 d = mk2(fma(sg, v[q].x, p.x), fma(sg, v[q].y, p.y));
+        if (st < 3) {
+          d = cmul(d, wst[st]);
+        } else if (st == 3) {
+          const double2 r = rot_mi(d, INV);
+          d = rot ? r : d;
+        }
+        v[q] = d;
+      }
     }
   }
 }
+
+template <int K>
+__device__ __forceinline__ int ring_out_index(int lane, int q);
 
 // 15-point DFT in registers, natural order in and out: prime-factor
 // (Good-Thomas) 3 x 5 with no twiddles -- input n = (5 na + 3 nb) mod 15,
@@ -235,14 +292,13 @@ __device__ void ring_fft15(double2* ring, const double2* tw) {
   __syncthreads();
   double2 wst[3];
   cross_twiddles<K, INV>(wst, tw, lane, 15);
-  const int b = (int)(__brev((unsigned)lane) >> 27);
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int k2 = warp + i * nw;
     if (k2 < 15) {
       ring_fft<K, INV>(c[i], tw, lane, wst, 15);
 #pragma unroll
-      for (int m1 = 0; m1 < K; ++m1) ring[pad_idx(k2 + 15 * (m1 + K * b))] = c[i][m1];
+      for (int m1 = 0; m1 < K; ++m1) ring[pad_idx(k2 + 15 * ring_out_index<K>(lane, m1))] = c[i][m1];
     }
   }
   __syncthreads();
@@ -341,10 +397,20 @@ __device__ __forceinline__ void ring_fft_q(double2 (&v)[K], const double2* tw, i
     for (int a = 0; a < 8; ++a) ring[pad_idx(q + 8 * c + K * (a + 8 * b))] = u[c][a];
 }
 
-// Output index held by (lane, slot m1) after ring_fft.
+// Output index held by (lane, slot q) after ring_fft.  Odd K: m1 = q and the
+// radix-2 DIF leaves m2 = brev5(lane).  Half exchange: each stage swapped its lane
+// bit with the register-half bit t = q >= K/2, so with b = brev5(lane) the column is
+// m1 = (b & 1) K/2 + (q mod K/2) and m2 = (b >> 1) + 16 t.
 template <int K>
-__device__ __forceinline__ int ring_out_index(int lane, int m1) {
-  return m1 + K * (int)(__brev((unsigned)lane) >> 27);
+__device__ __forceinline__ int ring_out_index(int lane, int q) {
+  const int b = (int)(__brev((unsigned)lane) >> 27);
+  if constexpr (half_exchange<K>()) {
+    constexpr int H = K / 2;
+    const int t = q >= H ? 1 : 0;
+    return (b & 1) * H + (q - t * H) + K * ((b >> 1) + 16 * t);
+  } else {
+    return q + K * b;
+  }
 }
 
 // Transform the warp's ring held in v (lane l: points 32 k + l) and store the

@@ -67,6 +67,10 @@ int launch_sweep_node(int R, const ModelConsts& c, double beta, const SpecCombin
                       double2* theta, double2* fi, long long nstates, cudaStream_t st);
 int launch_upload_triangle(const double2* host, double2* out, int R, long long nmat,
                            cudaStream_t st);
+// hostpack.cu: host-packed triangles, one contiguous copy-engine transfer, device expansion
+bool packed_upload_available();
+int pack_triangles_host(const double2* dense, int R, long long nmat, double2* packed);
+int launch_upload_packed(const double2* host, double2* out, int R, long long nmat, cudaStream_t st);
 int launch_download_triangle(const double2* dev, double2* host, int R, long long nmat,
                              int write_lower, cudaStream_t st);
 constexpr int kMaxExBlocks = 64;

@@ -141,6 +141,41 @@ def test_tma_and_forced_split_variants_match_reference(tmp_path):
         assert float(out.stdout.strip().splitlines()[-1]) < TOL, (env, out.stdout)
 
 
+def test_packed_upload_matches_host():
+    """SWSDC_UPLOAD_MODE=2 (host-packed triangles, stream gated by a stream memory
+    operation, one contiguous copy, device expansion): more batches than staging
+    slots, of changing size (slot reallocation), on two streams, each equal to the
+    host matrices with a zero lower triangle; small transfers keep the zero-copy
+    kernel.  The knob is read once per process, hence the subprocess."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, sys; sys.path.insert(0, '.');"
+        "from paper_1805_07923_b200 import spharm, _lib;"
+        "rng = np.random.default_rng(5); bad = 0\n"
+        "streams = [torch.cuda.Stream(), torch.cuda.Stream()]\n"
+        "n0 = _lib.launch_count()\n"
+        "jobs = []\n"
+        "for k, (R, nm) in enumerate([(255, 15), (255, 15), (127, 40), (255, 3), (255, 15), (170, 9),"
+        " (255, 15), (255, 15), (255, 15), (255, 30), (255, 15), (31, 2)]):\n"
+        "    c = rng.standard_normal((nm, R + 1, R + 1)) + 1j * rng.standard_normal((nm, R + 1, R + 1))\n"
+        "    host = torch.from_numpy(c).pin_memory()\n"
+        "    with torch.cuda.stream(streams[k % 2]):\n"
+        "        dev = spharm.upload_coeffs(host)\n"
+        "    jobs.append((c, host, dev))\n"
+        "torch.cuda.synchronize()\n"
+        "for c, host, dev in jobs:\n"
+        "    bad += not np.array_equal(dev.cpu().numpy(), np.triu(c))\n"
+        "print(bad)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for env in ({"SWSDC_UPLOAD_MODE": "2"}, {"SWSDC_UPLOAD_MODE": "2", "SWSDC_PACK_THREADS": "3"},
+                {"SWSDC_UPLOAD_MODE": "0"}, {"SWSDC_UPLOAD_MODE": "1"}):
+        out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True,
+                             text=True, env={**os.environ, **env}, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        assert int(out.stdout.strip().splitlines()[-1]) == 0, (env, out.stdout)
+
+
 @pytest.mark.parametrize("R,I,J", [(63, 1920, 96), (31, 3840, 48), (47, 1920, 73)])
 def test_long_rings_match_oracle(R, I, J):
     """n_lon = 15 * 32 K rings (T639 / T1279 grids: one latitude pair per CTA)

@@ -87,6 +87,23 @@ def test_c_abi_exports_every_declared_symbol():
     assert lib.swsdc_version().startswith(b"swsdc_b200")
 
 
+@pytest.mark.parametrize("R,nmat", [(0, 1), (5, 3), (63, 7), (255, 15)])
+def test_pack_triangles_host(R, nmat):
+    """Host half of the packed upload: the s >= r triangles row after row, whatever the
+    slicing over the packing threads (T255 x 15 is the config-1 batch: 16 slices)."""
+    lib = _lib.load()
+    rng = np.random.default_rng(R)
+    dense = rng.standard_normal((nmat, R + 1, R + 1)) + 1j * rng.standard_normal((nmat, R + 1, R + 1))
+    tri = np.triu_indices(R + 1)
+    packed = np.full((nmat, len(tri[0])), np.nan + 0j)
+    for _ in range(2):
+        assert lib.swsdc_pack_triangles(dense.ctypes.data_as(ctypes.c_void_p), R, nmat,
+                                        packed.ctypes.data_as(ctypes.c_void_p)) == 0
+        np.testing.assert_array_equal(packed, dense[:, tri[0], tri[1]])
+    assert lib.swsdc_pack_triangles(None, R, nmat, None) == 1
+    assert lib.swsdc_pack_triangles(None, R, 0, None) == 0
+
+
 def test_c_abi_usage_errors_need_no_gpu():
     lib = _lib.load()
     mu = np.zeros(8)
