@@ -411,6 +411,8 @@ __global__ void SWSDC_REG_BOUNDS(K) f2g_reg_kernel(PlanDev P, const double2* eo,
   }
   __syncthreads();
   // 2. each warp assembles its pair's packed spectrum in registers and transforms it
+  //    (the decimation-in-time variant with its gathered input order measured slower
+  //    here: 35.2 vs 27.1 us at config 1, profiles/r02/experiments.md)
   const int jhw = jh0 + warp;
   double2 v[K];
   double2 wst[3];
@@ -534,6 +536,13 @@ __global__ void SWSDC_REG_BOUNDS(K) g2f_reg_kernel(PlanDev P, const double* grid
   }
 }
 
+// Quad-split FFT (ring_fft_q) in the fused F_E kernels at K = 24; -DSWSDC_FFT_QUAD=0
+// builds them with the shuffle stages instead (same-box A/B).
+#ifndef SWSDC_FFT_QUAD
+#define SWSDC_FFT_QUAD 0
+#endif
+#define SWSDC_FFT_QUAD24(K) (SWSDC_FFT_QUAD != 0 && (K) == 24)
+
 // Output stage shared by the fused SWE kernels: weighted analysis vectors at
 // wavenumber r of latitude pair jh from its 7 (or 2) forward-transformed
 // product rings (natural order) into x.
@@ -619,7 +628,7 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
       double2 v[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
-      swfft::ring_fft_to<K, true, K == 24>(v, P.tw, lane, wst, ring);
+      swfft::ring_fft_to<K, true, SWSDC_FFT_QUAD24(K)>(v, P.tw, lane, wst, ring);
     }
   }
   __syncthreads();
@@ -654,7 +663,7 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
       double2 v[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
-      swfft::ring_fft_to<K, false, K == 24>(v, P.tw, lane, wst, ring);
+      swfft::ring_fft_to<K, false, SWSDC_FFT_QUAD24(K)>(v, P.tw, lane, wst, ring);
     }
   }
   __syncthreads();
@@ -801,6 +810,11 @@ __global__ void __launch_bounds__(kG5Threads, g5_min_blocks<K>()) swe_grid5_kern
   fill_g5(rings, cf, P, eo + (size_t)m * eo_mstride + (size_t)jh * 2, fstride);
   __syncthreads();
   GRID_STAMP(1);
+  // Inverse transforms decimate in frequency and leave each grid in the transform's
+  // own output order, stored register-major (slot q of lane l at 32 q + l: conflict-
+  // free, no padding); the products are pointwise, so they run in that order, and
+  // the forward transforms decimate in time from it (ring_fft_dit), ending in natural
+  // order for the output stage: no scatter through shared memory in either direction.
   if (warp < 4) {   // U/a, V/a, zeta, phi' to the grid
     double2 wst[3];
     swfft::cross_twiddles<K, true>(wst, P.tw, lane);
@@ -808,14 +822,16 @@ __global__ void __launch_bounds__(kG5Threads, g5_min_blocks<K>()) swe_grid5_kern
     double2 v[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
-    swfft::ring_fft_to<K, true, K == 24>(v, P.tw, lane, wst, ring);
+    swfft::ring_fft<K, true>(v, P.tw, lane, wst);
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < K; ++q) ring[32 * q + lane] = v[q];
   }
   __syncthreads();
   GRID_STAMP(2);
   const double mu = P.mu_n[jh];
   const double ic2 = 1.0 / (1.0 - mu * mu);   // swe.py:180
-  for (int il = threadIdx.x; il < P.I; il += blockDim.x) {
-    const int p = swfft::pad_idx(il);
+  for (int p = threadIdx.x; p < P.I; p += blockDim.x) {
     const double2 U = rings[p], V = rings[RS + p], Z = rings[2 * RS + p], Ph = rings[3 * RS + p];
     // swe.py:271-273 : Phi U, Phi V, zeta U, zeta V, KE = (U^2 + V^2) / (2 (1 - mu^2))
     rings[p] = d2(Ph.x * U.x, Ph.y * U.y);
@@ -828,12 +844,15 @@ __global__ void __launch_bounds__(kG5Threads, g5_min_blocks<K>()) swe_grid5_kern
   GRID_STAMP(3);
   {
     double2 wst[3];
-    swfft::cross_twiddles<K, false>(wst, P.tw, lane);
+    swfft::cross_twiddles_dit<K, false>(wst, P.tw, lane);
     double2* ring = rings + (size_t)warp * RS;
     double2 v[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
-    swfft::ring_fft_to<K, false, K == 24>(v, P.tw, lane, wst, ring);
+    for (int q = 0; q < K; ++q) v[q] = ring[32 * q + lane];
+    swfft::ring_fft_dit<K, false>(v, P.tw, lane, wst);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < K; ++k) ring[swfft::pad_idx(32 * k + lane)] = v[k];
   }
   __syncthreads();
   GRID_STAMP(4);

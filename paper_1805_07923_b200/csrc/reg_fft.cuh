@@ -230,6 +230,102 @@ __device__ __forceinline__ void ring_fft(double2 (&v)[K], const double2* tw, int
   }
 }
 
+// Decimation-in-time counterpart: the transpose of ring_fft.  Lane l enters with
+// y[ring_out_index<K>(l, q)] in v[q] (exactly what ring_fft leaves behind) and ends
+// with Y[32 k + l] in v[k]: the cross-lane stages run in reverse order (h = 1 .. 16,
+// butterflies a + w b, a - w b), then the twiddle W_N^(l m1), then the in-lane K-point
+// DFT (symmetric, so its own transpose).  A DIF transform followed by pointwise work
+// and a DIT transform needs no reordering in between, and a transform whose input is
+// gathered anyway (the packed spectrum of a latitude pair) ends in the order in which
+// rings are stored: neither scatters through shared memory.
+// wd from cross_twiddles_dit: W_{2h}^(l mod h), on every lane for the half exchange,
+// on the upper lane of each pair (1 on the lower) otherwise.
+template <int K, bool INV>
+__device__ __forceinline__ void cross_twiddles_dit(double2 (&wd)[3], const double2* tw, int lane,
+                                                   int tws = 1) {
+#pragma unroll
+  for (int st = 0; st < 3; ++st) {
+    const int h = 16 >> st;
+    const int j = lane & (h - 1);
+    const double2 w = tw_at(tw, j * (16 / h) * K * tws, INV);
+    wd[st] = (half_exchange<K>() || (lane & h)) ? w : mk2(1.0, 0.0);
+  }
+}
+
+template <int K, bool INV>
+__device__ __forceinline__ void ring_fft_dit(double2 (&v)[K], const double2* tw, int lane,
+                                             const double2 (&wd)[3], int tws = 1) {
+  if constexpr (half_exchange<K>()) {
+    constexpr int H = K / 2;
+#pragma unroll
+    for (int st = 4; st >= 0; --st) {
+      const int h = 16 >> st;
+      const bool up = (lane & h) != 0;
+      const bool rot = (st == 3) && (lane & 1);   // h = 2: W_4^1 on odd lanes
+#pragma unroll
+      for (int u = 0; u < H; ++u) {
+        double2 d = v[u + H];
+        if (st < 3) {
+          d = cmul(d, wd[st]);
+        } else if (st == 3) {
+          const double2 r = rot_mi(d, INV);
+          d = rot ? r : d;
+        }
+        const double2 a = mk2(v[u].x + d.x, v[u].y + d.y);
+        const double2 b = mk2(v[u].x - d.x, v[u].y - d.y);
+        // the lower lane keeps a (slot u) and takes the partner's a into slot u + H;
+        // the upper lane keeps b (slot u + H) and takes the partner's b into slot u
+        const double2 send = up ? a : b;
+        double2 p;
+        p.x = __shfl_xor_sync(kFull, send.x, h);
+        p.y = __shfl_xor_sync(kFull, send.y, h);
+        v[u] = up ? p : a;
+        v[u + H] = up ? b : p;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int st = 4; st >= 0; --st) {
+      const int h = 16 >> st;
+      const bool up = (lane & h) != 0;
+      const double sg = up ? -1.0 : 1.0;
+      const bool rot = (st == 3) && up && (lane & 1);
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        double2 t = v[q];
+        if (st < 3) {
+          t = cmul(t, wd[st]);
+        } else if (st == 3) {
+          const double2 r = rot_mi(t, INV);
+          t = rot ? r : t;
+        }
+        double2 p;
+        p.x = __shfl_xor_sync(kFull, t.x, h);
+        p.y = __shfl_xor_sync(kFull, t.y, h);
+        // lower lane: own + w partner; upper lane: partner - w own
+        v[q] = mk2(fma(sg, t.x, p.x), fma(sg, t.y, p.y));
+      }
+    }
+  }
+  constexpr int NB = K > 16 ? 5 : K > 8 ? 4 : K > 4 ? 3 : K > 2 ? 2 : 1;
+  double2 wp[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) wp[b] = tw_at(tw, (lane << b) * tws, INV);
+#pragma unroll
+  for (int m1 = 1; m1 < K; ++m1) {
+    double2 w = mk2(1.0, 0.0);
+    bool first = true;
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if ((m1 >> b) & 1) {
+        w = first ? wp[b] : cmul(w, wp[b]);
+        first = false;
+      }
+    v[m1] = cmul(v[m1], w);
+  }
+  dft_k<K, INV>(v, tw);
+}
+
 template <int K>
 __device__ __forceinline__ int ring_out_index(int lane, int q);
 
