@@ -361,6 +361,13 @@ __global__ void __launch_bounds__(256, 2) g2f_kernel(PlanDev P, const double* gr
 // analysis-layout writes (rings in natural order, padded); the transforms run
 // in registers with no CTA barriers between stages.
 // ---------------------------------------------------------------------------
+// Warp index as a value the compiler knows to be warp-uniform: code under
+// `if (warp < n)` then keeps plain shuffles (no divergence check with an
+// out-of-line WARPSYNC.COLLECTIVE path per shuffle).
+__device__ __forceinline__ int uniform_warp() {
+  return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+}
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
@@ -391,7 +398,7 @@ __global__ void SWSDC_REG_BOUNDS(K) f2g_reg_kernel(PlanDev P, const double2* eo,
   pdl_trigger();
   extern __shared__ __align__(16) double2 rings[];
   const int np = 1 << lnp;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = uniform_warp();
   const int f = blockIdx.y;
   const int jh0 = jh_begin + blockIdx.x * np;
   const int R = P.R, I = P.I, row = eo_row(np);
@@ -471,7 +478,7 @@ __global__ void SWSDC_REG_BOUNDS(K) g2f_reg_kernel(PlanDev P, const double* grid
   constexpr int NIN = (MODE == 0) ? 1 : 2;
   extern __shared__ __align__(16) double2 rings[];  // [NIN][np][RS], natural order
   const int np = 1 << lnp;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = uniform_warp();
   const int f = blockIdx.y;
   const int jh0 = blockIdx.x * np;
   const double* gin[2] = {grid + (size_t)f * grid_fstride,
@@ -804,7 +811,7 @@ __global__ void __launch_bounds__(kG5Threads, g5_min_blocks<K>()) swe_grid5_kern
   const int m = blockIdx.y;
   const int RS = P.ring_stride;
   double2* cf = rings + (size_t)kG5Rings * RS;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = uniform_warp();
   const size_t fstride = (size_t)(P.R + 1) * P.Jh * 2;
   GRID_STAMP(0);
   fill_g5(rings, cf, P, eo + (size_t)m * eo_mstride + (size_t)jh * 2, fstride);
@@ -822,7 +829,9 @@ __global__ void __launch_bounds__(kG5Threads, g5_min_blocks<K>()) swe_grid5_kern
     double2 v[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
+    GRID_STAMP(5);
     swfft::ring_fft<K, true>(v, P.tw, lane, wst);
+    GRID_STAMP(7);
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < K; ++q) ring[32 * q + lane] = v[q];
@@ -864,6 +873,7 @@ __global__ void __launch_bounds__(kG5Threads, g5_min_blocks<K>()) swe_grid5_kern
     double* xm = x + (size_t)m * xl.mstride;
     for (int r = threadIdx.x; r <= P.R; r += blockDim.x)
       swe_out_g5(rings, cf, P, xm, xl, r, jh, w, w * ic2, ia, 2.0 * omega * mu, c2o, eq);
+    GRID_STAMP(6);
   } else {
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
@@ -905,7 +915,7 @@ __global__ void __launch_bounds__(128) swe_fwd_reg_kernel(PlanDev P, const doubl
   extern __shared__ __align__(16) double2 rings[];  // [4][RS] product spectra
   const int jh = jh_begin + blockIdx.x, m = blockIdx.y, role = blockIdx.z;
   const int RS = P.ring_stride;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = uniform_warp();
   const int jn = jn_of(P, jh), js = js_of(P, jh);
   // this pair's ring of field q (U/a, V/a, zeta, delta, phi'): I contiguous (north, south);
   // the role's fields are staged whole (coalesced 16-byte async copies, all in

@@ -31,8 +31,10 @@ t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 t = np.where(t > 0, t - t0, -1)
 names = ["entry", "filled", "inverse", "products", "forward", "cluster", "output", "exit"]
-print(f"R={R} grid {I}x{J} members {M}: CTAs {len(t)}, span {t[:, 7].max()} ns")
-for a, b in [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 6), (6, 7), (0, 7)]:
+print(f"R={R} grid {I}x{J} members {M}: CTAs {len(t)}, span {t.max()} ns")
+for a, b in [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 6), (6, 7), (4, 6), (0, 6), (0, 7), (1, 5), (5, 7), (7, 2)]:
     m = (t[:, a] >= 0) & (t[:, b] >= 0)
     d = t[m, b] - t[m, a]
+    if d.size == 0:
+        continue
     print(f"  {names[a]:>8s} -> {names[b]:8s}: med {int(np.median(d)):7d} ns  p10 {int(np.percentile(d, 10)):7d}  p90 {int(np.percentile(d, 90)):7d}")
