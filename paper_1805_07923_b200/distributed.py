@@ -63,6 +63,21 @@ class ShardSpec:
         b0, b1 = self.block_bounds(q, jh4)
         return min(4 * b0, Jh), min(4 * b1, Jh)
 
+    def chunk_blocks(self, q: int, jh4: int, chunk: tuple[int, int] | None) -> tuple[int, int]:
+        """4-pair blocks of rank q's chunk (c, C): its block range cut into C pieces
+        (every rank uses the same C, so chunk c of one rank travels in the same
+        collective as chunk c of every other rank; pieces may be empty)."""
+        b0, b1 = self.block_bounds(q, jh4)
+        if chunk is None:
+            return b0, b1
+        c, C = chunk
+        n = b1 - b0
+        return b0 + (n * c) // C, b0 + (n * (c + 1)) // C
+
+    def chunk_lats(self, q: int, jh4: int, Jh: int, chunk: tuple[int, int] | None) -> tuple[int, int]:
+        b0, b1 = self.chunk_blocks(q, jh4, chunk)
+        return min(4 * b0, Jh), min(4 * b1, Jh)
+
 
 class TorchExchanger:
     """Collectives over torch.distributed: NCCL all_to_all / all_gather /
@@ -187,9 +202,11 @@ def _blocks(arr: torch.Tensor, outer: int, rows: int, cols: int, inner: int, blo
     scatter the buffer back -- one library launch."""
     nb = len(blocks)
     arrs = [(ctypes.c_int * nb)(*[b[i] for b in blocks]) for i in range(5)]
+    n = sum(outer * b[2] * (b[4] - b[3]) * inner for b in blocks)
     if buf is None:
-        n = sum(outer * b[2] * (b[4] - b[3]) * inner for b in blocks)
         buf = torch.empty(n, dtype=torch.float64, device=arr.device)
+    if n == 0:
+        return buf
     _lib.check(_lib.load().swsdc_exchange_blocks(_ptr(arr), outer, rows, cols, inner, nb, *arrs,
                                                  _ptr(buf), 1 if scatter else 0,
                                                  _stream_ptr(arr.device)))
@@ -200,74 +217,84 @@ def _seg_sizes(outer, inner, blocks):
     return [outer * b[2] * (b[4] - b[3]) * inner for b in blocks]
 
 
-def exchange_eo(ex, spec: ShardSpec, eo: torch.Tensor, R: int, Jh: int, jh4: int) -> torch.Tensor:
+def exchange_eo(ex, spec: ShardSpec, eo: torch.Tensor, R: int, Jh: int, jh4: int,
+                chunk: tuple[int, int] | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
     """eo [m, 5, R+1, Jh, 4] with valid own rows -> same shape with ALL rows valid
     for this rank's latitude pairs.  Device tensors: one pack launch, one flat
     all-to-all, one unpack launch (swsdc_exchange_blocks); host tensors (the gloo
-    CPU tests) take the equivalent torch slicing below."""
+    CPU tests) take the equivalent torch slicing below.  chunk = (c, C) moves only
+    piece c of every rank's latitude range (into `out`, shared by the C calls), so
+    the grid stage of piece c can run while piece c + 1 is in flight."""
     P = spec.P
     if eo.is_cuda and hasattr(ex, "all_to_all_flat"):
         m, f = eo.shape[0], eo.shape[1]
         arr = eo.contiguous()
         nmine = len(range(spec.rank, R + 1, P))
-        sblocks = [(spec.rank, P, nmine, *spec.lat_bounds(q, jh4, Jh)) for q in range(P)]
-        j0, j1 = spec.lat_bounds(spec.rank, jh4, Jh)
+        sblocks = [(spec.rank, P, nmine, *spec.chunk_lats(q, jh4, Jh, chunk)) for q in range(P)]
+        j0, j1 = spec.chunk_lats(spec.rank, jh4, Jh, chunk)
         rblocks = [(p, P, len(range(p, R + 1, P)), j0, j1) for p in range(P)]
         sbuf = _blocks(arr, m * f, R + 1, Jh, 4, sblocks, None, False)
         rs = _seg_sizes(m * f, 4, rblocks)
         rbuf = torch.empty(sum(rs), dtype=torch.float64, device=eo.device)
         ex.all_to_all_flat(sbuf, _seg_sizes(m * f, 4, sblocks), rbuf, rs)
-        out = torch.empty_like(arr)
+        if out is None:
+            out = torch.empty_like(arr)
         _blocks(out, m * f, R + 1, Jh, 4, rblocks, rbuf, True)
         return out
     rows = spec.rows(R)
     sends, shapes = [], []
     m = eo.shape[0]
     for q in range(P):
-        j0, j1 = spec.lat_bounds(q, jh4, Jh)
+        j0, j1 = spec.chunk_lats(q, jh4, Jh, chunk)
         sends.append(eo[:, :, rows, j0:j1, :])
-    j0, j1 = spec.lat_bounds(spec.rank, jh4, Jh)
+    j0, j1 = spec.chunk_lats(spec.rank, jh4, Jh, chunk)
     for p in range(P):
         nrows = len(range(p, R + 1, P))
         shapes.append((m, eo.shape[1], nrows, j1 - j0, 4))
     recvs = ex.all_to_all(sends, shapes)
-    out = torch.empty_like(eo)
+    if out is None:
+        out = torch.empty_like(eo)
     for p in range(P):
         out[:, :, p:R + 1:P, j0:j1, :] = recvs[p]
     return out
 
 
-def exchange_x(ex, spec: ShardSpec, x: torch.Tensor, R: int, jh4: int) -> torch.Tensor:
+def exchange_x(ex, spec: ShardSpec, x: torch.Tensor, R: int, jh4: int,
+               chunk: tuple[int, int] | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
     """x [m, G, R+1, jh4, F] (fragment-native analysis input, F = 2*nc*4) valid for
     all rows on this rank's latitude blocks -> same shape valid for own rows on
-    ALL latitude blocks (device tensors: library pack / flat all-to-all / unpack)."""
+    ALL latitude blocks (device tensors: library pack / flat all-to-all / unpack).
+    chunk = (c, C): only piece c of every rank's block range (into `out`), sent
+    while the grid stage works on piece c + 1."""
     P = spec.P
     if x.is_cuda and hasattr(ex, "all_to_all_flat"):
         m, G, F = x.shape[0], x.shape[1], x.shape[-1]
         arr = x.contiguous()
-        b0, b1 = spec.block_bounds(spec.rank, jh4)
+        b0, b1 = spec.chunk_blocks(spec.rank, jh4, chunk)
         sblocks = [(p, P, len(range(p, R + 1, P)), b0, b1) for p in range(P)]
         nmine = len(range(spec.rank, R + 1, P))
-        rblocks = [(spec.rank, P, nmine, *spec.block_bounds(q, jh4)) for q in range(P)]
+        rblocks = [(spec.rank, P, nmine, *spec.chunk_blocks(q, jh4, chunk)) for q in range(P)]
         sbuf = _blocks(arr, m * G, R + 1, jh4, F, sblocks, None, False)
         rs = _seg_sizes(m * G, F, rblocks)
         rbuf = torch.empty(sum(rs), dtype=torch.float64, device=x.device)
         ex.all_to_all_flat(sbuf, _seg_sizes(m * G, F, sblocks), rbuf, rs)
-        out = torch.empty_like(arr)
+        if out is None:
+            out = torch.empty_like(arr)
         _blocks(out, m * G, R + 1, jh4, F, rblocks, rbuf, True)
         return out
     sends, shapes = [], []
-    b0, b1 = spec.block_bounds(spec.rank, jh4)
+    b0, b1 = spec.chunk_blocks(spec.rank, jh4, chunk)
     for p in range(P):
         sends.append(x[:, :, p:R + 1:P, b0:b1, :])
     nrows = len(range(spec.rank, R + 1, P))
     for q in range(P):
-        c0, c1 = spec.block_bounds(q, jh4)
+        c0, c1 = spec.chunk_blocks(q, jh4, chunk)
         shapes.append(tuple(x.shape[:2]) + (nrows, c1 - c0, x.shape[-1]))
     recvs = ex.all_to_all(sends, shapes)
-    out = torch.empty_like(x)
+    if out is None:
+        out = torch.empty_like(x)
     for q in range(P):
-        c0, c1 = spec.block_bounds(q, jh4)
+        c0, c1 = spec.chunk_blocks(q, jh4, chunk)
         out[:, :, spec.rank:R + 1:P, c0:c1, :] = recvs[q]
     return out
 
@@ -307,9 +334,14 @@ class ShardedRHS(ShallowWaterRHS):
     library call of the sweep (solve, F_I, combines, restriction, FAS,
     interpolation) is row-filtered too."""
 
-    def __init__(self, plan, params, exchanger, spec: ShardSpec, include_nonlinear: bool = True):
+    def __init__(self, plan, params, exchanger, spec: ShardSpec, include_nonlinear: bool = True,
+                 chunks: int = 4):
         super().__init__(plan, params, include_nonlinear)
         self.ex, self.spec = exchanger, spec
+        # pieces of each rank's latitude range: exchanges of one piece run on a side
+        # stream while the grid stage works on another (1 = the unpipelined order)
+        self.chunks = max(1, int(chunks))
+        self._comm = None
         lib = _lib.load()
         eo_n, x_n, nc, jh4 = ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_int(), ctypes.c_int()
         _lib.check(lib.swsdc_fe_layout(plan.handle, 1 if include_nonlinear else 0, 1,
@@ -333,15 +365,52 @@ class ShardedRHS(ShallowWaterRHS):
         st = _stream_ptr(dev)
         eo = torch.empty(m * self.eo_per, dtype=torch.float64, device=dev)
         _lib.check(lib.swsdc_fe_synthesis(self.plan.handle, cp, _ptr(x), m, _ptr(eo), st))
-        eo_full = exchange_eo(self.ex, self.spec, eo.view(m, 5, R + 1, self.Jh, 4), R, self.Jh,
-                              self.jh4)
-        j0, j1 = self.spec.lat_bounds(self.spec.rank, self.jh4, self.Jh)
+        eo_v = eo.view(m, 5, R + 1, self.Jh, 4)
         xb = torch.empty(m * self.x_per, dtype=torch.float64, device=dev)
-        _lib.check(lib.swsdc_fe_grid(self.plan.handle, cp, nl, _ptr(eo_full), m, j0, j1, _ptr(xb),
-                                     st))
         groups = self.x_per // ((R + 1) * self.jh4 * 2 * self.nc * 4)
         xv = xb.view(m, groups, R + 1, self.jh4, 2 * self.nc * 4)
-        x_full = exchange_x(self.ex, self.spec, xv, R, self.jh4).contiguous()
+        C = self.chunks
+        if C == 1 or not x.is_cuda:
+            eo_full = exchange_eo(self.ex, self.spec, eo_v, R, self.Jh, self.jh4)
+            j0, j1 = self.spec.lat_bounds(self.spec.rank, self.jh4, self.Jh)
+            _lib.check(lib.swsdc_fe_grid(self.plan.handle, cp, nl, _ptr(eo_full), m, j0, j1,
+                                         _ptr(xb), st))
+            x_full = exchange_x(self.ex, self.spec, xv, R, self.jh4).contiguous()
+        else:
+            # Pipeline over C pieces of the latitude range: the side
+            # stream carries pack -> all-to-all -> unpack of one piece while the main
+            # stream runs the grid stage of another.  Every rank issues the same
+            # sequence of collectives: E/O pieces 0..C-1, then the x piece behind each
+            # grid piece.  Exposed communication: the first E/O piece and the last x
+            # piece; the analysis (a reduction over all latitudes) waits for all of x.
+            main = torch.cuda.current_stream(dev)
+            if self._comm is None:
+                self._comm = torch.cuda.Stream(device=dev)
+            comm = self._comm
+            eo_full = torch.empty_like(eo_v)
+            x_full = torch.empty_like(xv)
+            ready = torch.cuda.Event()
+            ready.record(main)
+            ev_eo = [torch.cuda.Event() for _ in range(C)]
+            with torch.cuda.stream(comm):
+                comm.wait_event(ready)
+                for c in range(C):
+                    exchange_eo(self.ex, self.spec, eo_v, R, self.Jh, self.jh4, (c, C), eo_full)
+                    ev_eo[c].record(comm)
+            for c in range(C):
+                j0, j1 = self.spec.chunk_lats(self.spec.rank, self.jh4, self.Jh, (c, C))
+                main.wait_event(ev_eo[c])
+                if j1 > j0:
+                    _lib.check(lib.swsdc_fe_grid(self.plan.handle, cp, nl, _ptr(eo_full), m, j0, j1,
+                                                 _ptr(xb), st))
+                done = torch.cuda.Event()
+                done.record(main)
+                with torch.cuda.stream(comm):
+                    comm.wait_event(done)
+                    exchange_x(self.ex, self.spec, xv, R, self.jh4, (c, C), x_full)
+            fin = torch.cuda.Event()
+            fin.record(comm)
+            main.wait_event(fin)
         out = torch.empty_like(x)
         _lib.check(lib.swsdc_fe_analysis(self.plan.handle, cp, nl, _ptr(x_full), m, _ptr(out), st))
         return PrognosticState.from_tensor(out)
@@ -349,14 +418,14 @@ class ShardedRHS(ShallowWaterRHS):
 
 def sharded_hierarchy(params, r_fine, nodes_fine, r_coarse, nodes_coarse, exchanger,
                       spec: ShardSpec, grid_fine=None, grid_coarse=None, device=None,
-                      include_nonlinear: bool = True):
+                      include_nonlinear: bool = True, chunks: int = 4):
     """build_hierarchy with ShardedRHS on both levels."""
     from . import mlsdc
     base = mlsdc.build_hierarchy(params, r_fine, nodes_fine, r_coarse, nodes_coarse,
                                  include_nonlinear, grid_fine, grid_coarse, device)
     lv = []
     for level in (base.fine, base.coarse):
-        rhs = ShardedRHS(level.plan, params, exchanger, spec, include_nonlinear)
+        rhs = ShardedRHS(level.plan, params, exchanger, spec, include_nonlinear, chunks)
         lv.append(mlsdc.Level(plan=level.plan, tables=level.tables, rhs=rhs))
     return mlsdc.TwoLevelHierarchy(fine=lv[0], coarse=lv[1], ops=base.ops)
 

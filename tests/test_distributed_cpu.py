@@ -52,6 +52,19 @@ def _worker(rank, world, port, R, Jh, fails):
         x[:, :, :, b0:b1] = xt[:, :, :, b0:b1]
         xf = exchange_x(ex, spec, x, R, jh4)
         assert torch.equal(xf[:, :, rank:R + 1:world], xt[:, :, rank:R + 1:world]), "x exchange"
+        # --- pipelined form: C pieces of every rank's latitude range, one collective each,
+        #     assembled into one buffer (C = 5 leaves some pieces empty at small Jh)
+        for C in (2, 3, 5):
+            full_c = torch.full_like(truth, float("nan"))
+            xf_c = torch.full_like(xt, float("nan"))
+            for c in range(C):
+                exchange_eo(ex, spec, eo, R, Jh, jh4, (c, C), full_c)
+                exchange_x(ex, spec, x, R, jh4, (c, C), xf_c)
+            assert torch.equal(full_c[:, :, :, j0:j1], truth[:, :, :, j0:j1]), f"eo pieces C={C}"
+            assert torch.equal(xf_c[:, :, rank:R + 1:world], xt[:, :, rank:R + 1:world]), f"x pieces C={C}"
+            pieces = [spec.chunk_blocks(rank, jh4, (c, C)) for c in range(C)]
+            assert pieces[0][0] == b0 and pieces[-1][1] == b1
+            assert all(pieces[c][1] == pieces[c + 1][0] for c in range(C - 1))
         # --- gather_state
         st = torch.randn(3, 3, R + 1, R + 1, dtype=torch.complex128, generator=torch.Generator().manual_seed(7))
         mine = torch.full_like(st, complex(float("nan"), 0.0))

@@ -1,6 +1,8 @@
 """m-sharded MLSDC (distributed.py) on ONE GPU: P virtual ranks run as threads
 with host-side exchanges (no kernel waits on another); the gathered state must
-match the unsharded oracle step."""
+match the unsharded oracle step.  chunks > 1: the F_E exchanges travel in pieces
+of the latitude range on a side stream while the grid stage works on other pieces
+(chunks = 7 leaves some pieces empty on the coarse level's 6 blocks)."""
 
 import threading
 
@@ -14,8 +16,8 @@ from conftest import rel_err
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("P", [2, 3])
-def test_sharded_mlsdc_step_matches_oracle(P):
+@pytest.mark.parametrize("P,chunks", [(2, 4), (3, 2), (2, 1), (3, 7)])
+def test_sharded_mlsdc_step_matches_oracle(P, chunks):
     from paper_1805_07923_b200 import distributed as D
     from paper_1805_07923_b200 import swe, workloads
     params = swe.ModelParams(**workloads.EARTH)
@@ -28,7 +30,7 @@ def test_sharded_mlsdc_step_matches_oracle(P):
             ex = hub.view(rank)
             spec = D.ShardSpec(P, rank)
             hier = D.sharded_hierarchy(params, 31, 5, 15, 3, ex, spec, grid_fine=(96, 48),
-                                       grid_coarse=(48, 24))
+                                       grid_coarse=(48, 24), chunks=chunks)
             st = swe.PrognosticState(torch.as_tensor(x).cuda())
             y = D.sharded_mlsdc_timestep(st, 240.0, 2, hier, spec, n_coarse_sweeps=2)
             results[rank] = D.gather_state(ex, spec, y.data).cpu().numpy()
