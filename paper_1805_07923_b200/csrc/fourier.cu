@@ -368,6 +368,17 @@ __device__ __forceinline__ int uniform_warp() {
   return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
 }
 
+// 32-byte global accesses (sm_100 LDG / STG .256): one sector, one LSU data-pipe
+// wavefront, where two 16-byte accesses of the same sector cost two.
+__device__ __forceinline__ void ld_global_256(const double2* p, double2& a, double2& b) {
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p));
+}
+__device__ __forceinline__ void st_global_256(double* p, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y) : "memory");
+}
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
@@ -732,9 +743,7 @@ __device__ __forceinline__ void fill_g5(double2* rings, double2* cf, const PlanD
     double2 E[5], O[5];
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
-      const double2* src = eo + q * fstride + (size_t)r * P.Jh * 2;
-      E[q] = src[0];
-      O[q] = src[1];
+      ld_global_256(eo + q * fstride + (size_t)r * P.Jh * 2, E[q], O[q]);
     }
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
@@ -784,15 +793,34 @@ __device__ __forceinline__ void swe_out_g5(const double2* rings, const double2* 
   const double2 A2s = d2(-fn * Zs.x - c2o * Us.x, -fn * Zs.y - c2o * Us.y);
   const double rwa = r * wc * ia, wa = wc * ia;
   // P-vectors: phi, zeta, delta, ke ; H-vectors: phi, zeta, delta
-  put_x(xm, xl, 0, r, jh, ir_scale(PUn, -rwa), ir_scale(PUs, -rwa), eq);
-  put_x(xm, xl, 1, r, jh, cadd2(cscale(A1n, w), ir_scale(ZUn, -rwa)),
-        cadd2(cscale(A1s, w), ir_scale(ZUs, -rwa)), eq);
-  put_x(xm, xl, 2, r, jh, cadd2(cscale(A2n, w), ir_scale(ZVn, rwa)),
-        cadd2(cscale(A2s, w), ir_scale(ZVs, rwa)), eq);
-  put_x(xm, xl, 3, r, jh, cscale(Kn, w), cscale(Ks, w), eq);
-  put_x(xm, xl, 4, r, jh, cscale(PVn, wa), cscale(PVs, wa), eq);
-  put_x(xm, xl, 5, r, jh, cscale(ZVn, wa), cscale(ZVs, wa), eq);
-  put_x(xm, xl, 6, r, jh, cscale(ZUn, wa), cscale(ZUs, wa), eq);
+  const double2 vn[7] = {ir_scale(PUn, -rwa), cadd2(cscale(A1n, w), ir_scale(ZUn, -rwa)),
+                         cadd2(cscale(A2n, w), ir_scale(ZVn, rwa)), cscale(Kn, w),
+                         cscale(PVn, wa), cscale(ZVn, wa), cscale(ZUn, wa)};
+  const double2 vs[7] = {ir_scale(PUs, -rwa), cadd2(cscale(A1s, w), ir_scale(ZUs, -rwa)),
+                         cadd2(cscale(A2s, w), ir_scale(ZVs, rwa)), cscale(Ks, w),
+                         cscale(PVs, wa), cscale(ZVs, wa), cscale(ZUs, wa)};
+  if (xl.pm) {
+    // pair-major: the 16 columns of (r, jh, parity) are one 128-byte row -- four
+    // 32-byte stores per parity (vector pairs; column 14-15 is padding, zeroed)
+    double2 S[8], D[8];
+#pragma unroll
+    for (int v = 0; v < 7; ++v) {
+      S[v] = eq ? vn[v] : d2(vn[v].x + vs[v].x, vn[v].y + vs[v].y);
+      D[v] = eq ? d2(0.0, 0.0) : d2(vn[v].x - vs[v].x, vn[v].y - vs[v].y);
+    }
+    S[7] = d2(0.0, 0.0);
+    D[7] = d2(0.0, 0.0);
+    double* rs = xm + xl.idx(0, 0, r, jh, 0);
+    double* rd = xm + xl.idx(0, 0, r, jh, 1);
+#pragma unroll
+    for (int v = 0; v < 8; v += 2) {
+      st_global_256(rs + 2 * v, S[v], S[v + 1]);
+      st_global_256(rd + 2 * v, D[v], D[v + 1]);
+    }
+    return;
+  }
+#pragma unroll
+  for (int v = 0; v < 7; ++v) put_x(xm, xl, v, r, jh, vn[v], vs[v], eq);
 }
 
 template <int K>
@@ -811,9 +839,11 @@ __global__ void __launch_bounds__(kG5Threads, g5_min_blocks<K>()) swe_grid5_kern
   const int m = blockIdx.y;
   const int RS = P.ring_stride;
   double2* cf = rings + (size_t)kG5Rings * RS;
+  double2* twc = cf + 8 * (size_t)(P.R + 1);          // twiddle cache (reg_fft.cuh)
   const int lane = threadIdx.x & 31, warp = uniform_warp();
   const size_t fstride = (size_t)(P.R + 1) * P.Jh * 2;
   GRID_STAMP(0);
+  swfft::fill_twiddle_cache<K>(twc, P.tw, threadIdx.x, blockDim.x);
   fill_g5(rings, cf, P, eo + (size_t)m * eo_mstride + (size_t)jh * 2, fstride);
   __syncthreads();
   GRID_STAMP(1);
@@ -824,14 +854,12 @@ __global__ void __launch_bounds__(kG5Threads, g5_min_blocks<K>()) swe_grid5_kern
   // order for the output stage: no scatter through shared memory in either direction.
   if (warp < 4) {   // U/a, V/a, zeta, phi' to the grid
     double2 wst[3];
-    swfft::cross_twiddles<K, true>(wst, P.tw, lane);
+    swfft::cross_twiddles<K, true, true>(wst, twc, lane);
     double2* ring = rings + (size_t)warp * RS;
     double2 v[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
-    GRID_STAMP(5);
-    swfft::ring_fft<K, true>(v, P.tw, lane, wst);
-    GRID_STAMP(7);
+    swfft::ring_fft<K, true, true>(v, twc, lane, wst);
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < K; ++q) ring[32 * q + lane] = v[q];
@@ -853,12 +881,12 @@ __global__ void __launch_bounds__(kG5Threads, g5_min_blocks<K>()) swe_grid5_kern
   GRID_STAMP(3);
   {
     double2 wst[3];
-    swfft::cross_twiddles_dit<K, false>(wst, P.tw, lane);
+    swfft::cross_twiddles_dit<K, false, true>(wst, twc, lane);
     double2* ring = rings + (size_t)warp * RS;
     double2 v[K];
 #pragma unroll
     for (int q = 0; q < K; ++q) v[q] = ring[32 * q + lane];
-    swfft::ring_fft_dit<K, false>(v, P.tw, lane, wst);
+    swfft::ring_fft_dit<K, false, true>(v, twc, lane, wst);
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < K; ++k) ring[swfft::pad_idx(32 * k + lane)] = v[k];
@@ -1394,7 +1422,8 @@ int swe_reg_launch(const PlanDev& P, const double2* eo, long long eo_mstride, do
   const bool cl = cl_knob && !xl.pm && (jh_begin % 4 == 0) && ((jh_end - jh_begin) % 4 == 0);
   static const int g5 = env_int("SWSDC_SWE_G5", 1);   // 0: the 12-FFT kernel below
   if (NONLIN && g5) {
-    const size_t smem5 = sizeof(double2) * ((size_t)kG5Rings * P.ring_stride + 8 * (P.R + 1));
+    const size_t smem5 = sizeof(double2) * ((size_t)kG5Rings * P.ring_stride + 8 * (P.R + 1) +
+                                           swfft::tw_cache_entries<K>());
     StageScope sc("swe_grid", st);
     if (cl) {
       SW_TRY(set_smem((const void*)swe_grid5_kernel<K, true>, smem5));

@@ -136,33 +136,78 @@ __host__ __device__ constexpr bool half_exchange() { return SWSDC_FFT_HX != 0 &&
 // formed as own - partner.
 // tws: stride of tw relative to an N-point table (a sub-transform of a longer
 // ring reads the longer ring's table: W_N^e = tw[e * tws]).
-template <int K, bool INV>
+//
+// Twiddle cache (TWC): the lane-gathered table reads of one transform -- the powers
+// W_N^(lane 2^b), b < NB, and the three stage twiddles -- touch ~9 K sectors, one
+// LSU wavefront each, and every warp of a CTA gathers the same values.  A CTA that
+// runs several transforms fills a [NB + 3][32] cache in shared memory once
+// (fill_twiddle_cache) and its transforms read their lane's entries from it (4
+// wavefronts per read); `tw` is then the cache, forward values, conjugated on use.
+template <int K>
+__host__ __device__ constexpr int tw_powers() { return K > 16 ? 5 : K > 8 ? 4 : K > 4 ? 3 : K > 2 ? 2 : 1; }
+template <int K>
+__host__ __device__ constexpr int tw_cache_entries() { return (tw_powers<K>() + 3) * 32; }
+
+template <int K>
+__device__ __forceinline__ void fill_twiddle_cache(double2* cache, const double2* tw, int tid,
+                                                   int nthreads) {
+  constexpr int NB = tw_powers<K>();
+  for (int i = tid; i < (NB + 3) * 32; i += nthreads) {
+    const int e = i >> 5, lane = i & 31;
+    int idx;
+    if (e < NB) {
+      idx = lane << e;
+    } else {
+      const int h = 16 >> (e - NB);
+      idx = (lane & (h - 1)) * (16 / h) * K;
+    }
+    cache[i] = tw[idx];
+  }
+}
+
+// stage twiddle W_{2h}^(lane mod h), h = 16 >> st
+template <int K, bool INV, bool TWC>
+__device__ __forceinline__ double2 stage_twiddle(const double2* tw, int lane, int st, int tws) {
+  if constexpr (TWC) {
+    return tw_at(tw, (tw_powers<K>() + st) * 32 + lane, INV);
+  } else {
+    const int h = 16 >> st;
+    return tw_at(tw, (lane & (h - 1)) * (16 / h) * K * tws, INV);
+  }
+}
+// power W_N^(lane 2^b)
+template <int K, bool INV, bool TWC>
+__device__ __forceinline__ double2 power_twiddle(const double2* tw, int lane, int b, int tws) {
+  if constexpr (TWC) return tw_at(tw, b * 32 + lane, INV);
+  else return tw_at(tw, (lane << b) * tws, INV);
+}
+
+template <int K, bool INV, bool TWC = false>
 __device__ __forceinline__ void cross_twiddles(double2 (&wst)[3], const double2* tw, int lane,
                                                int tws = 1) {
 #pragma unroll
   for (int st = 0; st < 3; ++st) {
     const int h = 16 >> st;
-    const int j = lane & (h - 1);
     if constexpr (half_exchange<K>()) {
-      const double2 w = tw_at(tw, j * (16 / h) * K * tws, INV);
+      const double2 w = stage_twiddle<K, INV, TWC>(tw, lane, st, tws);
       wst[st] = (lane & h) ? mk2(-w.x, -w.y) : w;
     } else {
-      wst[st] = (lane & h) ? tw_at(tw, j * (16 / h) * K * tws, INV) : mk2(1.0, 0.0);
+      wst[st] = (lane & h) ? stage_twiddle<K, INV, TWC>(tw, lane, st, tws) : mk2(1.0, 0.0);
     }
   }
 }
 
 // Full N-point transform (see the header comment); wst from cross_twiddles.
-template <int K, bool INV>
+template <int K, bool INV, bool TWC = false>
 __device__ __forceinline__ void ring_fft(double2 (&v)[K], const double2* tw, int lane,
                                          const double2 (&wst)[3], int tws = 1) {
   dft_k<K, INV>(v, tw);
   // W_N^(lane m1) from the gathered powers W_N^(lane 2^b) (2^b < K, so
   // lane 2^b < N) by at most 4 products: 5 table gathers instead of K - 1
-  constexpr int NB = K > 16 ? 5 : K > 8 ? 4 : K > 4 ? 3 : K > 2 ? 2 : 1;
+  constexpr int NB = tw_powers<K>();
   double2 wp[NB];
 #pragma unroll
-  for (int b = 0; b < NB; ++b) wp[b] = tw_at(tw, (lane << b) * tws, INV);
+  for (int b = 0; b < NB; ++b) wp[b] = power_twiddle<K, INV, TWC>(tw, lane, b, tws);
 #pragma unroll
   for (int m1 = 1; m1 < K; ++m1) {
     double2 w = mk2(1.0, 0.0);
@@ -240,19 +285,18 @@ __device__ __forceinline__ void ring_fft(double2 (&v)[K], const double2* tw, int
 // rings are stored: neither scatters through shared memory.
 // wd from cross_twiddles_dit: W_{2h}^(l mod h), on every lane for the half exchange,
 // on the upper lane of each pair (1 on the lower) otherwise.
-template <int K, bool INV>
+template <int K, bool INV, bool TWC = false>
 __device__ __forceinline__ void cross_twiddles_dit(double2 (&wd)[3], const double2* tw, int lane,
                                                    int tws = 1) {
 #pragma unroll
   for (int st = 0; st < 3; ++st) {
     const int h = 16 >> st;
-    const int j = lane & (h - 1);
-    const double2 w = tw_at(tw, j * (16 / h) * K * tws, INV);
+    const double2 w = stage_twiddle<K, INV, TWC>(tw, lane, st, tws);
     wd[st] = (half_exchange<K>() || (lane & h)) ? w : mk2(1.0, 0.0);
   }
 }
 
-template <int K, bool INV>
+template <int K, bool INV, bool TWC = false>
 __device__ __forceinline__ void ring_fft_dit(double2 (&v)[K], const double2* tw, int lane,
                                              const double2 (&wd)[3], int tws = 1) {
   if constexpr (half_exchange<K>()) {
@@ -307,10 +351,10 @@ __device__ __forceinline__ void ring_fft_dit(double2 (&v)[K], const double2* tw,
       }
     }
   }
-  constexpr int NB = K > 16 ? 5 : K > 8 ? 4 : K > 4 ? 3 : K > 2 ? 2 : 1;
+  constexpr int NB = tw_powers<K>();
   double2 wp[NB];
 #pragma unroll
-  for (int b = 0; b < NB; ++b) wp[b] = tw_at(tw, (lane << b) * tws, INV);
+  for (int b = 0; b < NB; ++b) wp[b] = power_twiddle<K, INV, TWC>(tw, lane, b, tws);
 #pragma unroll
   for (int m1 = 1; m1 < K; ++m1) {
     double2 w = mk2(1.0, 0.0);
