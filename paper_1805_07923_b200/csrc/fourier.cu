@@ -392,6 +392,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // E/O staging row stride (double2) for np pairs: 2 np + 1 keeps the lanes'
 // reads of consecutive wavenumbers in distinct bank groups.
 __host__ __device__ inline int eo_row(int np) { return 2 * np + 1; }
+// f2g_reg_kernel: double2 slots of the staging / rings region
+__host__ __device__ inline size_t f2g_reg_elems(const PlanDev& P, int np) {
+  const size_t a = (size_t)np * P.ring_stride, b = (size_t)(P.R + 1) * eo_row(np);
+  return a > b ? a : b;
+}
 
 // K >= 16: 4 pairs (128 threads) per CTA, registers capped for 3 CTAs/SM;
 // smaller rings: up to 8 pairs (256 threads).
@@ -735,7 +740,8 @@ constexpr int kG5Threads = 160;
 
 // Fill rings 0..3 with the packed spectra of fields U, V, zeta, phi' (eo
 // fields 0, 1, 2, 4) and cf[q][r] = (F_n, F_s) of fields U, V, zeta, delta
-// (eo fields 0..3) with Im dropped at r = 0, as the grid round trip would.
+// (eo fields 0..3) with Im dropped at r = 0, as the grid round trip would
+// (cf[2 q + side][r], so consecutive lanes touch consecutive 16-byte slots).
 __device__ __forceinline__ void fill_g5(double2* rings, double2* cf, const PlanDev& P,
                                         const double2* eo, size_t fstride) {
   const int R = P.R, I = P.I, RS = P.ring_stride, nt = blockDim.x;
@@ -751,8 +757,8 @@ __device__ __forceinline__ void fill_g5(double2* rings, double2* cf, const PlanD
         double2 Fn = d2(E[q].x + O[q].x, E[q].y + O[q].y);
         double2 Fs = d2(E[q].x - O[q].x, E[q].y - O[q].y);
         if (r == 0) { Fn.y = 0.0; Fs.y = 0.0; }
-        cf[2 * (q * (R + 1) + r)] = Fn;
-        cf[2 * (q * (R + 1) + r) + 1] = Fs;
+        cf[(2 * q) * (R + 1) + r] = Fn;        // [field][north | south][r]: lanes 16 B apart
+        cf[(2 * q + 1) * (R + 1) + r] = Fs;
       }
       if (q == 3) continue;            // no delta ring
       const int ring = q == 4 ? 3 : q;
@@ -782,10 +788,10 @@ __device__ __forceinline__ void swe_out_g5(const double2* rings, const double2* 
   get_pair(rings + 2 * RS, P, r, ZUn, ZUs);
   get_pair(rings + 3 * RS, P, r, ZVn, ZVs);
   get_pair(rings + 4 * RS, P, r, Kn, Ks);
-  const double2 Un = cf[2 * r], Us = cf[2 * r + 1];
-  const double2 Vn = cf[2 * (R1 + r)], Vs = cf[2 * (R1 + r) + 1];
-  const double2 Zn = cf[2 * (2 * R1 + r)], Zs = cf[2 * (2 * R1 + r) + 1];
-  const double2 Dn = cf[2 * (3 * R1 + r)], Ds = cf[2 * (3 * R1 + r) + 1];
+  const double2 Un = cf[r], Us = cf[R1 + r];
+  const double2 Vn = cf[2 * R1 + r], Vs = cf[3 * R1 + r];
+  const double2 Zn = cf[4 * R1 + r], Zs = cf[5 * R1 + r];
+  const double2 Dn = cf[6 * R1 + r], Ds = cf[7 * R1 + r];
   // swe.py:262,265 in Fourier space; f = fn north, -fn south
   const double2 A1n = d2(-fn * Dn.x - c2o * Vn.x, -fn * Dn.y - c2o * Vn.y);
   const double2 A1s = d2(fn * Ds.x - c2o * Vs.x, fn * Ds.y - c2o * Vs.y);
@@ -1283,8 +1289,7 @@ template <int K>
 int f2g_reg_launch(const PlanDev& P, const double2* eo, long long eo_fstride, double* grid,
                    long long grid_fstride, int nf, int jh_begin, int jh_end, cudaStream_t st) {
   const int lnp = pairs_log2(P, 1), np = 1 << lnp;
-  const size_t smem = sizeof(double2) * std::max((size_t)np * P.ring_stride,
-                                                 (size_t)(P.R + 1) * eo_row(np));
+  const size_t smem = sizeof(double2) * f2g_reg_elems(P, np);
   SW_TRY(set_smem((const void*)f2g_reg_kernel<K>, smem));
   dim3 gridDim((jh_end - jh_begin + np - 1) / np, nf);
   if (gridDim.x == 0) return kOk;
@@ -1505,11 +1510,10 @@ int launch_swe_split_reg(const PlanDev& P, bool nonlinear, const double2* eo, lo
   const long long gfield = (long long)P.Jh * P.I;   // double2 per field ring block
   const int lnp = pairs_log2(P, 1), np = 1 << lnp;
   dim3 g1((jh_end - jh_begin + np - 1) / np, 5 * nmembers);
-  const size_t smem1 = sizeof(double2) * std::max((size_t)np * P.ring_stride,
-                                                  (size_t)(P.R + 1) * eo_row(np));
   int st1 = kOk;
   auto first = [&](auto kk) -> int {
     constexpr int KK = decltype(kk)::value;
+    const size_t smem1 = sizeof(double2) * f2g_reg_elems(P, np);
     SW_TRY(set_smem((const void*)f2g_reg_kernel<KK, true>, smem1));
     StageScope sc("fourier_to_grid", st);
     SW_CUDA(launch_pdl(f2g_reg_kernel<KK, true>, dim3(g1), dim3(32 * np), smem1, st, P, eo, eo_fstride, reinterpret_cast<double*>(ring_ws), gfield, lnp, jh_begin, jh_end));

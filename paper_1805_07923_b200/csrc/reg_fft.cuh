@@ -559,13 +559,14 @@ __device__ __forceinline__ int ring_out_index(int lane, int q) {
 // was loaded from.  Measured per kernel (profiles/r01/experiments.md): the quad
 // split wins in the fused F_E grid kernel at K = 24 and loses at K = 16 / 8
 // and in the standalone f2g / g2f kernels.
-template <int K, bool INV, bool QUAD = false>
+template <int K, bool INV, bool QUAD = false, bool TWC = false>
 __device__ __forceinline__ void ring_fft_to(double2 (&v)[K], const double2* tw, int lane,
                                             const double2 (&wst)[3], double2* ring) {
   if constexpr (QUAD && K % 8 == 0) {
+    static_assert(!TWC, "the quad split reads the plan table");
     ring_fft_q<K, INV>(v, tw, lane, ring);
   } else {
-    ring_fft<K, INV>(v, tw, lane, wst);
+    ring_fft<K, INV, TWC>(v, tw, lane, wst);
     __syncwarp();
 #pragma unroll
     for (int m1 = 0; m1 < K; ++m1) ring[pad_idx(ring_out_index<K>(lane, m1))] = v[m1];
