@@ -299,6 +299,13 @@ __device__ __forceinline__ void stage_chunk(const ChunkRegs<B, MODE>& c, double2
   }
 }
 
+// (E, O) of one (field, row, latitude pair): one 32-byte sector, written with one
+// 256-bit store (two 16-byte stores would pass the LSU data stage twice)
+__device__ __forceinline__ void st_eo(double2* p, double2 e, double2 o) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "d"(e.x), "d"(e.y), "d"(o.x), "d"(o.y) : "memory");
+}
+
 template <int B>
 __device__ __forceinline__ void flush_row(double2 (&E)[B][kSynNL], double2 (&O)[B][kSynNL],
                                           double2* dst, int lane) {
@@ -424,8 +431,7 @@ syn_kernel(PlanDev P, SynArgs a) {
         for (int l = 0; l < kSynNL; ++l) {
           if (jh[l] < P.Jh) {
             double2* o = a.eo + (((size_t)b * (P.R + 1) + r) * P.Jh + jh[l]) * 2;
-            o[0] = E[b][l];
-            o[1] = O[b][l];
+            st_eo(o, E[b][l], O[b][l]);
           }
           E[b][l] = make_double2(0.0, 0.0);
           O[b][l] = make_double2(0.0, 0.0);
@@ -447,8 +453,7 @@ syn_kernel(PlanDev P, SynArgs a) {
         for (int l = 0; l < kSynNL; ++l)
           if (jh[l] < P.Jh) {
             double2* o = a.eo + (((size_t)b * (P.R + 1) + r) * P.Jh + jh[l]) * 2;
-            o[0] = E[b][l];
-            o[1] = O[b][l];
+            st_eo(o, E[b][l], O[b][l]);
           }
       return;
     }
@@ -465,8 +470,7 @@ syn_kernel(PlanDev P, SynArgs a) {
         o.x += src[1].x; o.y += src[1].y;
       }
       double2* dst = a.eo + (((size_t)b * (P.R + 1) + r) * P.Jh + j) * 2;
-      dst[0] = e;
-      dst[1] = o;
+      st_eo(dst, e, o);
     }
   }
 }
