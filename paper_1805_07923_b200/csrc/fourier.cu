@@ -89,6 +89,17 @@ __device__ __forceinline__ double2 cscale(double2 a, double s) { return d2(a.x *
 __device__ __forceinline__ double2 ir_scale(double2 a, double rs) { return d2(-a.y * rs, a.x * rs); }
 __device__ __forceinline__ double2 cadd2(double2 a, double2 b) { return d2(a.x + b.x, a.y + b.y); }
 
+// 32-byte global accesses (sm_100 LDG / STG .256): one sector, one LSU data-pipe
+// wavefront, where two 16-byte accesses of the same sector cost two.
+__device__ __forceinline__ void ld_global_256(const double2* p, double2& a, double2& b) {
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p));
+}
+__device__ __forceinline__ void st_global_256(double* p, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y) : "memory");
+}
+
 // Packed ring values at +r and -r from a pair's (E, O) partial sums.
 __device__ __forceinline__ void pair_spectrum(double2 E, double2 O, int r, double2& zp,
                                               double2& zm) {
@@ -122,9 +133,7 @@ __device__ __forceinline__ void fill_rings_pair(double2* rings, const PlanDev& P
       for (int q = 0; q < NR; ++q) {
         E[h][q] = O[h][q] = d2(0.0, 0.0);
         if (r <= R) {
-          const double2* src = eo + q * fstride + (size_t)r * P.Jh * 2;
-          E[h][q] = src[0];
-          O[h][q] = src[1];
+          ld_global_256(eo + q * fstride + (size_t)r * P.Jh * 2, E[h][q], O[h][q]);
         }
       }
     }
@@ -167,9 +176,7 @@ __device__ __forceinline__ void fill_rings(double2* rings, const PlanDev& P, con
         const int i = idx & (np - 1), qr = idx >> lnp;
         const int q = qr / (R + 1), r = qr - q * (R + 1);
         if (jh0 + i < P.Jh) {
-          const double2* src = eo + q * fstride + ((size_t)r * P.Jh + jh0 + i) * 2;
-          E[u] = src[0];
-          O[u] = src[1];
+          ld_global_256(eo + q * fstride + ((size_t)r * P.Jh + jh0 + i) * 2, E[u], O[u]);
         }
       }
     }
@@ -366,17 +373,6 @@ __global__ void __launch_bounds__(256, 2) g2f_kernel(PlanDev P, const double* gr
 // out-of-line WARPSYNC.COLLECTIVE path per shuffle).
 __device__ __forceinline__ int uniform_warp() {
   return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
-}
-
-// 32-byte global accesses (sm_100 LDG / STG .256): one sector, one LSU data-pipe
-// wavefront, where two 16-byte accesses of the same sector cost two.
-__device__ __forceinline__ void ld_global_256(const double2* p, double2& a, double2& b) {
-  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
-               : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p));
-}
-__device__ __forceinline__ void st_global_256(double* p, double2 a, double2 b) {
-  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
-               :: "l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y) : "memory");
 }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -1174,8 +1170,8 @@ __global__ void __launch_bounds__(256, 1) swe_prod_kernel(PlanDev P, const doubl
   // as the grid round trip would): eo fields U/a, V/a, zeta, delta, phi'
   const double2* em = eo + (size_t)m * 5 * eo_fstride + (size_t)jh * 2;
   auto coef = [&](int q, int r, double2& Fn, double2& Fs) {
-    const double2* e = em + (size_t)q * eo_fstride + (size_t)r * P.Jh * 2;
-    const double2 E = e[0], O = e[1];
+    double2 E, O;
+    ld_global_256(em + (size_t)q * eo_fstride + (size_t)r * P.Jh * 2, E, O);
     Fn = d2(E.x + O.x, r == 0 ? 0.0 : E.y + O.y);
     Fs = d2(E.x - O.x, r == 0 ? 0.0 : E.y - O.y);
   };
