@@ -870,18 +870,44 @@ __global__ void __launch_bounds__(kG5Threads, g5_min_blocks<K>()) swe_grid5_kern
   GRID_STAMP(2);
   const double mu = P.mu_n[jh];
   const double ic2 = 1.0 / (1.0 - mu * mu);   // swe.py:180
-  for (int p = threadIdx.x; p < P.I; p += blockDim.x) {
-    const double2 U = rings[p], V = rings[RS + p], Z = rings[2 * RS + p], Ph = rings[3 * RS + p];
-    // swe.py:271-273 : Phi U, Phi V, zeta U, zeta V, KE = (U^2 + V^2) / (2 (1 - mu^2))
-    rings[p] = d2(Ph.x * U.x, Ph.y * U.y);
-    rings[RS + p] = d2(Ph.x * V.x, Ph.y * V.y);
-    rings[2 * RS + p] = d2(Z.x * U.x, Z.y * U.y);
-    rings[3 * RS + p] = d2(Z.x * V.x, Z.y * V.y);
-    rings[4 * RS + p] = d2(0.5 * (U.x * U.x + V.x * V.x) * ic2, 0.5 * (U.y * U.y + V.y * V.y) * ic2);
-  }
-  __syncthreads();
-  GRID_STAMP(3);
-  {
+  if constexpr (K >= 20) {
+    // Products formed in registers on the way into the forward transforms (swe.py:271-273):
+    // warp w reads its two factor grids in transform order and multiplies pointwise --
+    // Phi U, Phi V, zeta U, zeta V, KE = (U^2 + V^2) / (2 (1 - mu^2)) -- instead of a
+    // separate pass that rewrites the rings; every read ends before any ring is rewritten.
+    // Measured per ring length: config 2 (K = 24) -1.5%, config 4 (K = 16 / 8) +0.4%, so
+    // the shorter rings keep the separate pass below.
+    double2 wst[3];
+    swfft::cross_twiddles_dit<K, false, true>(wst, twc, lane);
+    const int fa = (warp == 4) ? 0 : (warp < 2 ? 3 : 2);       // Phi', Phi', zeta, zeta, U
+    const int fb = (warp == 4) ? 1 : (warp & 1);               // U, V, U, V, V
+    const double2* ra = rings + (size_t)fa * RS;
+    const double2* rb = rings + (size_t)fb * RS;
+    double2 v[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      const double2 a = ra[32 * q + lane], b = rb[32 * q + lane];
+      v[q] = (warp == 4) ? d2(0.5 * (a.x * a.x + b.x * b.x) * ic2, 0.5 * (a.y * a.y + b.y * b.y) * ic2)
+                         : d2(a.x * b.x, a.y * b.y);
+    }
+    __syncthreads();
+    GRID_STAMP(3);
+    double2* ring = rings + (size_t)warp * RS;
+    swfft::ring_fft_dit<K, false, true>(v, twc, lane, wst);
+#pragma unroll
+    for (int k = 0; k < K; ++k) ring[swfft::pad_idx(32 * k + lane)] = v[k];
+  } else {
+    for (int p = threadIdx.x; p < P.I; p += blockDim.x) {
+      const double2 U = rings[p], V = rings[RS + p], Z = rings[2 * RS + p], Ph = rings[3 * RS + p];
+      // swe.py:271-273 : Phi U, Phi V, zeta U, zeta V, KE = (U^2 + V^2) / (2 (1 - mu^2))
+      rings[p] = d2(Ph.x * U.x, Ph.y * U.y);
+      rings[RS + p] = d2(Ph.x * V.x, Ph.y * V.y);
+      rings[2 * RS + p] = d2(Z.x * U.x, Z.y * U.y);
+      rings[3 * RS + p] = d2(Z.x * V.x, Z.y * V.y);
+      rings[4 * RS + p] = d2(0.5 * (U.x * U.x + V.x * V.x) * ic2, 0.5 * (U.y * U.y + V.y * V.y) * ic2);
+    }
+    __syncthreads();
+    GRID_STAMP(3);
     double2 wst[3];
     swfft::cross_twiddles_dit<K, false, true>(wst, twc, lane);
     double2* ring = rings + (size_t)warp * RS;
