@@ -555,13 +555,6 @@ __global__ void SWSDC_REG_BOUNDS(K) g2f_reg_kernel(PlanDev P, const double* grid
   }
 }
 
-// Quad-split FFT (ring_fft_q) in the fused F_E kernels at K = 24; -DSWSDC_FFT_QUAD=0
-// builds them with the shuffle stages instead (same-box A/B).
-#ifndef SWSDC_FFT_QUAD
-#define SWSDC_FFT_QUAD 0
-#endif
-#define SWSDC_FFT_QUAD24(K) (SWSDC_FFT_QUAD != 0 && (K) == 24)
-
 // Output stage shared by the fused SWE kernels: weighted analysis vectors at
 // wavenumber r of latitude pair jh from its 7 (or 2) forward-transformed
 // product rings (natural order) into x.
@@ -647,7 +640,7 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
       double2 v[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
-      swfft::ring_fft_to<K, true, SWSDC_FFT_QUAD24(K)>(v, P.tw, lane, wst, ring);
+      swfft::ring_fft_to<K, true>(v, P.tw, lane, wst, ring);
     }
   }
   __syncthreads();
@@ -682,7 +675,7 @@ __global__ void __launch_bounds__((K) >= 20 ? 192 : (K) == 16 ? 224 : 256, 2) sw
       double2 v[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) v[k] = ring[swfft::pad_idx(32 * k + lane)];
-      swfft::ring_fft_to<K, false, SWSDC_FFT_QUAD24(K)>(v, P.tw, lane, wst, ring);
+      swfft::ring_fft_to<K, false>(v, P.tw, lane, wst, ring);
     }
   }
   __syncthreads();

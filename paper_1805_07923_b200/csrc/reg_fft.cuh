@@ -4,9 +4,11 @@
 //   X[m] = sum_l W_32^(l m2) W_N^(l m1) sum_k x[32 k + l] W_K^(k m1),
 // so the transform is (A) a K-point DFT over the lane's own registers,
 // (B) the twiddle W_N^(l m1) on slot m1, (C) a 32-point DFT across the lanes
-// (radix-2 decimation in frequency over shfl.xor).  Afterwards lane l holds
-// X[m1 + K brev5(l)] in v[m1].  No shared memory and no barriers: the only
-// latency is the shuffles', and every stage has K independent chains.
+// (radix-2 decimation in frequency over shfl.xor; half exchanges for even K,
+// see below).  Afterwards slot q of lane l holds X[ring_out_index(l, q)]
+// (odd K: X[q + K brev5(l)]).  No shared memory and no barriers: the only
+// latency is the shuffles', and every stage has K (or K/2) independent chains.
+// ring_fft_dit is the transposed transform (input in that order, natural out).
 //
 // Twiddles come from the plan table tw[e] = exp(-2 pi i e / N) (capi.cu),
 // conjugated for the inverse: W_K^e = tw[32 e], W_32^e = tw[K e].
@@ -450,93 +452,6 @@ __host__ __device__ constexpr int fft15_k(int n) {
                            n / 480 == 16)) ? n / 480 : 0;
 }
 
-// Variant for K % 8 == 0 that replaces the five shuffle stages of the
-// 32-point cross-lane DFT by a transpose through the warp's ring (shared
-// memory) and a 4 x 8 split: with l = 4 i + j, m2 = a + 8 b,
-//   X[m1 + K m2] = sum_j W_4^(j b) W_32^(j a) sum_i B[4i + j][m1] W_8^(i a).
-// Quad q (lanes 4q .. 4q+3) takes the columns m1 = q + 8 c; lane j of the
-// quad runs the 8-point DFT over i in registers, twiddles by W_32^(j a), and
-// the quad finishes with a 4-point DFT over two shuffle stages (lane j ends
-// with b = bitrev2(j)).  Shuffles per lane: 4 K (two stages) instead of 10 K
-// (five), no redundant twiddle products on the lower lanes.  The result is
-// written to ring in natural order (padded slots); ring must not be read by
-// other lanes during the call (the caller loaded v from it, or owns it).
-// Transpose rows have stride 34 double2: conflict-free writes, 4 wavefronts
-// per quad-strided read (the minimum for 512 bytes).
-template <int K, bool INV>
-__device__ __forceinline__ void ring_fft_q(double2 (&v)[K], const double2* tw, int lane,
-                                           double2* ring) {
-  static_assert(K % 8 == 0, "quad split needs K % 8 == 0");
-  constexpr int TS = 34;
-  dft_k<K, INV>(v, tw);
-  constexpr int NB = K > 16 ? 5 : K > 8 ? 4 : 3;
-  double2 wp[NB];
-#pragma unroll
-  for (int b = 0; b < NB; ++b) wp[b] = tw_at(tw, lane << b, INV);
-#pragma unroll
-  for (int m1 = 1; m1 < K; ++m1) {
-    double2 w = mk2(1.0, 0.0);
-    bool first = true;
-#pragma unroll
-    for (int b = 0; b < NB; ++b)
-      if ((m1 >> b) & 1) {
-        w = first ? wp[b] : cmul(w, wp[b]);
-        first = false;
-      }
-    v[m1] = cmul(v[m1], w);
-  }
-  __syncwarp();   // every lane has finished reading ring (the caller's loads)
-#pragma unroll
-  for (int m1 = 0; m1 < K; ++m1) ring[m1 * TS + lane] = v[m1];
-  __syncwarp();
-  const int q = lane >> 2, j = lane & 3;
-  constexpr int C = K / 8;
-  double2 u[C][8];
-#pragma unroll
-  for (int c = 0; c < C; ++c)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) u[c][i] = ring[(q + 8 * c) * TS + 4 * i + j];
-  __syncwarp();   // transpose consumed: ring is free for the results
-  double2 wj[8];
-#pragma unroll
-  for (int a = 1; a < 8; ++a) wj[a] = tw_at(tw, K * j * a, INV);   // W_32^(j a)
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    small_dft<8>(u[c], INV);
-#pragma unroll
-    for (int a = 1; a < 8; ++a) u[c][a] = cmul(u[c][a], wj[a]);
-  }
-  // 4-point DFT across the quad: h = 2 (upper lanes j = 2, 3 take the
-  // difference, j = 3 also W_4^1), then h = 1
-  const double sg2 = (lane & 2) ? -1.0 : 1.0, sg1 = (lane & 1) ? -1.0 : 1.0;
-  const bool rot = (lane & 3) == 3;
-#pragma unroll
-  for (int c = 0; c < C; ++c)
-#pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      double2 p;
-      p.x = __shfl_xor_sync(kFull, u[c][a].x, 2);
-      p.y = __shfl_xor_sync(kFull, u[c][a].y, 2);
-      double2 d = mk2(fma(sg2, u[c][a].x, p.x), fma(sg2, u[c][a].y, p.y));
-      const double2 r = rot_mi(d, INV);
-      u[c][a] = rot ? r : d;
-    }
-#pragma unroll
-  for (int c = 0; c < C; ++c)
-#pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      double2 p;
-      p.x = __shfl_xor_sync(kFull, u[c][a].x, 1);
-      p.y = __shfl_xor_sync(kFull, u[c][a].y, 1);
-      u[c][a] = mk2(fma(sg1, u[c][a].x, p.x), fma(sg1, u[c][a].y, p.y));
-    }
-  const int b = ((j & 1) << 1) | (j >> 1);
-#pragma unroll
-  for (int c = 0; c < C; ++c)
-#pragma unroll
-    for (int a = 0; a < 8; ++a) ring[pad_idx(q + 8 * c + K * (a + 8 * b))] = u[c][a];
-}
-
 // Output index held by (lane, slot q) after ring_fft.  Odd K: m1 = q and the
 // radix-2 DIF leaves m2 = brev5(lane).  Half exchange: each stage swapped its lane
 // bit with the register-half bit t = q >= K/2, so with b = brev5(lane) the column is
@@ -554,23 +469,18 @@ __device__ __forceinline__ int ring_out_index(int lane, int q) {
 }
 
 // Transform the warp's ring held in v (lane l: points 32 k + l) and store the
-// spectrum to ring in natural order (padded slots): the quad split when QUAD
-// (K % 8 == 0), otherwise the five-stage shuffle FFT.  ring may be the buffer v
-// was loaded from.  Measured per kernel (profiles/r01/experiments.md): the quad
-// split wins in the fused F_E grid kernel at K = 24 and loses at K = 16 / 8
-// and in the standalone f2g / g2f kernels.
-template <int K, bool INV, bool QUAD = false, bool TWC = false>
+// spectrum to ring in natural order (padded slots).  ring may be the buffer v
+// was loaded from.  (A quad-split variant -- the 32-point cross-lane DFT as a
+// transpose through the ring, in-lane 8-point DFTs and two shuffle stages --
+// won in the fused F_E kernel at K = 24 against full-exchange shuffle stages and
+// lost to the half exchange: profiles/r01 and r02 experiments.md.)
+template <int K, bool INV, bool TWC = false>
 __device__ __forceinline__ void ring_fft_to(double2 (&v)[K], const double2* tw, int lane,
                                             const double2 (&wst)[3], double2* ring) {
-  if constexpr (QUAD && K % 8 == 0) {
-    static_assert(!TWC, "the quad split reads the plan table");
-    ring_fft_q<K, INV>(v, tw, lane, ring);
-  } else {
-    ring_fft<K, INV, TWC>(v, tw, lane, wst);
-    __syncwarp();
+  ring_fft<K, INV, TWC>(v, tw, lane, wst);
+  __syncwarp();
 #pragma unroll
-    for (int m1 = 0; m1 < K; ++m1) ring[pad_idx(ring_out_index<K>(lane, m1))] = v[m1];
-  }
+  for (int m1 = 0; m1 < K; ++m1) ring[pad_idx(ring_out_index<K>(lane, m1))] = v[m1];
 }
 
 }  // namespace swfft
