@@ -278,9 +278,14 @@ def run_ours(args, world, rank, local):
     import torch
     from paper_1805_07923_b200 import _lib, spharm, workloads
 
+    # test hooks for exercising the N > 1 path on a one-GPU box: every rank on cuda:0
+    # and a gloo group (exchanges staged through host memory, so no kernel of one rank
+    # waits on another's); the driver's runs use neither
+    if os.environ.get("SWSDC_BENCH_SHARE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist = init_dist(world, "nccl")
+    dist = init_dist(world, os.environ.get("SWSDC_BENCH_BACKEND", "nccl"))
 
     plan = spharm.TransformPlan(spharm.build_gaussian_grid(J, I), R, device=dev)
     plan.reserve(NF)
