@@ -208,6 +208,39 @@ def test_long_rings_match_oracle(R, I, J):
         assert rel_err(fe[f], ofe[f]) < TOL
 
 
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24])
+@pytest.mark.parametrize("members", [1, 3])
+def test_every_register_fft_length_matches_oracle(K, members):
+    """Every ring length with a register FFT (n_lon = 32 K): the half-exchange
+    shuffle stages (even K) and the full-exchange ones (odd K), decimation in
+    frequency (f2g / g2f, the fused kernel's inverse transforms) and in time (its
+    forward transforms), at truncations that fill the band (3/2 rule) on a few
+    latitudes, single states and ensembles -- against the numpy oracle."""
+    import swsdc_oracle as orc
+    from paper_1805_07923_b200 import spharm, swe, workloads
+    I = 32 * K
+    R = max(1, min((I - 1) // 3, 42))
+    J = 10
+    plan = plan_for(R, I, J)
+    oplan = orc.OraclePlan(R, I, J)
+    c = workloads.transform_batch(R, 2)
+    g = plan.synthesize(torch.as_tensor(c).cuda()).cpu().numpy()
+    want = np.stack([oplan.synthesize(ci) for ci in c])
+    assert rel_err(g, want) < TOL
+    back = plan.analyze(torch.as_tensor(want).cuda()).cpu().numpy()
+    assert rel_err(back, np.stack([oplan.analyze(gi) for gi in want])) < TOL
+    params = swe.ModelParams(**workloads.EARTH)
+    orhs = orc.OracleRHS(oplan, orc.OracleParams(**workloads.EARTH))
+    x = np.stack([workloads.seeded_state(R, k) for k in range(members)])
+    fe = swe.ShallowWaterRHS(plan, params).eval_f_e(
+        swe.PrognosticState(torch.as_tensor(x if members > 1 else x[0]).cuda())).numpy()
+    fe = fe if members > 1 else fe[None]
+    for m in range(members):
+        ofe = orhs.eval_fe(x[m])
+        for f in range(3):
+            assert rel_err(fe[m][f], ofe[f]) < TOL, (m, f)
+
+
 def test_round2_kernel_variants_match_reference():
     """Round-2 alternatives behind knobs (read once per process, so each runs in a
     subprocess): the opt-in tensor-core synthesis (SWSDC_SYN_DMMA=1, 4/8/16 fields
