@@ -8,6 +8,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 from conftest import ROOT
 
 
@@ -40,3 +42,31 @@ def test_reference_arm_line():
 def test_reference_arm_only_rank_zero_prints():
     """Under torchrun (N > 1) rank 0 alone runs and prints the reference line."""
     assert _run({"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"}) == []
+
+
+@pytest.mark.gpu
+def test_gpu_arm_line():
+    """The GPU arm's line on a short run: the headline config, a roofline object for the
+    dominant kernel measured live, an end-to-end number with its transfer bytes, the
+    library's own launch count and the clocks sampled during the timed region."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3",
+                          "--warmup", "3", "--soak", "0", "--no-cpu-baseline", "--no-mlsdc"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = out.stdout.strip().splitlines()
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["metric"] == "SH transform pairs/s (fp64)" and d["unit"] == "field-pairs/s"
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["dtype"] == "f64" and d["scaling"] == "weak"
+    assert d["config"]["workload"].startswith("config1:") and d["vs_baseline"] is None
+    assert d["value"] > 1e4 and d["gpu_launches"] >= 4 * 3
+    r = d["roofline"]
+    assert r["bound"] in ("hbm", "tensor") and r["unit"] in ("GB/s", "TFLOP/s")
+    assert 0.0 < r["frac"] < 1.0 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    e = d["e2e"]
+    tri = 15 * 256 * 257 // 2 * 16
+    assert e["h2d_bytes_per_step"] == tri and e["d2h_bytes_per_step"] == tri
+    assert 0 < e["value"] < d["value"] and e["roundtrip_err"] < 1e-12
+    c = d["clocks"]
+    assert c["sm_mhz"] > 0 and c["sm_max_mhz"] >= c["sm_mhz"] and isinstance(c["reasons"], list)
+    assert d["roundtrip_err"] < 1e-12
