@@ -440,7 +440,13 @@ int launch_combine(const CombineArgs& a, long long count, cudaStream_t st) {
 int launch_spec_combine_multi(const MultiCombineArgs& a, long long nmat, cudaStream_t st) {
   if (a.nout <= 0 || nmat <= 0) return kOk;
   const int row = a.rout + 1;
-  const int threads = row >= 256 ? 256 : ((row + 31) / 32) * 32;
+  // the grid covers the largest output extent, not the array size: an in-place
+  // interpolation into fine arrays only touches the coarse (r, s) square (config 4:
+  // the 6-output interpolation launch ran 197k CTAs of which 3/4 of the threads
+  // returned at once, 146 us at 2.6 TB/s)
+  int ext = 0;
+  for (int o = 0; o < a.nout; ++o) ext = std::max(ext, std::min(a.ext[o], a.rout) + 1);
+  const int threads = ext >= 256 ? 256 : ((ext + 31) / 32) * 32;
   // gridDim.z = nout x matrices <= 65535: larger batches go in matrix chunks,
   // each launch with its inputs / outputs advanced to the chunk's first matrix
   const long long per = std::max(1LL, 65535LL / a.nout);
@@ -452,7 +458,7 @@ int launch_spec_combine_multi(const MultiCombineArgs& a, long long nmat, cudaStr
       c.x[k] = a.x[k] + (size_t)m0 * (a.rin[k] + 1) * (a.rin[k] + 1);
     for (int o = 0; o < a.nout; ++o) c.out[o] = a.out[o] + (size_t)m0 * row * row;
     SW_CUDA(launch_pdl(spec_combine_multi_kernel,
-                       dim3((row + threads - 1) / threads, row, (unsigned)(a.nout * nm)),
+                       dim3((ext + threads - 1) / threads, ext, (unsigned)(a.nout * nm)),
                        dim3(threads), 0, st, c, nm, current_row_filter()));
     SW_LAUNCH_CHECK();
   }
