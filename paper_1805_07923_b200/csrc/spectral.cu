@@ -380,6 +380,11 @@ __global__ void sweep_node_kernel(int R, ModelConsts c, double beta, SpecCombine
   fi[o + 2 * plane] = make_double2(-lam * ph.x + nl * de.x, -lam * ph.y + nl * de.y);
 }
 
+// Threads per row block of the (s, r, matrix) grids: the row length rounded up to a
+// warp (<= 256), so a 171- or 86-entry row is one 192- or 96-thread block instead of two
+// blocks with a third of their threads idle.
+int row_threads(int row) { return row >= 256 ? 256 : ((row + 31) / 32) * 32; }
+
 int grid_for(long long n, int threads) {
   long long b = (n + threads - 1) / threads;
   if (b > 148 * 16) b = 148 * 16;
@@ -393,7 +398,7 @@ int launch_finalize_swe(const PlanDev& P, const double2* Y, long long y_mstride,
                         double2* out, long long out_mstride, bool nonlin, double radius,
                         int nmembers, cudaStream_t st, RowFilter rf) {
   if (nmembers <= 0) return kOk;
-  const int tx = P.R + 1 >= 128 ? 128 : 64;
+  const int tx = row_threads(P.R + 1);
   const dim3 grid((P.R + 1 + tx - 1) / tx, P.R + 1, nmembers);
   StageScope sc("finalize_swe", st);
   SW_CUDA(launch_pdl(finalize_swe_kernel, grid, dim3(tx), 0, st, P, Y, y_mstride, ldy, out, out_mstride, nonlin ? 1 : 0, radius, nmembers, rf));
@@ -413,7 +418,7 @@ int launch_finalize_divcurl(const PlanDev& P, const double2* Y, long long y_mstr
 int launch_eval_fi(int R, const ModelConsts& c, const double2* x, double2* out, long long nmat,
                    cudaStream_t st) {
   if (nmat <= 0) return kOk;
-  const int tx = R + 1 >= 128 ? 128 : 64;
+  const int tx = row_threads(R + 1);
   const dim3 grid((R + 1 + tx - 1) / tx, R + 1, (unsigned)nmat);
   StageScope sc("eval_fi", st);
   SW_CUDA(launch_pdl(eval_fi_kernel, grid, dim3(tx), 0, st, R, c, x, out, nmat, current_row_filter()));
@@ -487,7 +492,7 @@ int launch_spec_combine(const SpecCombineArgs& a, long long nmat, cudaStream_t s
 int launch_sweep_node(int R, const ModelConsts& c, double beta, const SpecCombineArgs& a,
                       double2* theta, double2* fi, long long nstates, cudaStream_t st) {
   if (nstates <= 0) return kOk;
-  const int tx = R + 1 >= 128 ? 128 : 64;
+  const int tx = row_threads(R + 1);
   const dim3 grid((R + 1 + tx - 1) / tx, R + 1, (unsigned)nstates);
   StageScope sc("sweep_node", st);
   SW_CUDA(launch_pdl(sweep_node_kernel, grid, dim3(tx), 0, st, R, c, beta, a, theta, fi, nstates, current_row_filter()));
